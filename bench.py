@@ -1,0 +1,361 @@
+"""CPR-GMRES SOLVE benchmark (BASELINE.json metric) on the SPE10-shaped system.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--grid 60,220,85] [--cycle v|k]
+
+One step = one complete CPR-GMRES solve (build_cpr done beforehand, as the
+reference times SETUP and SOLVE separately, src/cpr.py:369-376) of the
+synthetic 60x220x85 three-phase black-oil Jacobian (3,366,000 DOF, 3x3 BSR,
+seed 0, drift 0.01) with SolverConfig(theta=0, theta_amg=0, cycle='v').
+`value` is the device time-to-solution in ms (inputs resident in HBM; the
+working set, > 1 GB, exceeds the 126 MB L2 so no flush is needed).  `e2e`
+is the same solve through the public API from pinned host buffers.
+`--impl reference` times the CPU oracle (oracle/cprkit_oracle.py, a numpy
+restatement of the reference) on the host cores.  For N > 1 every rank solves
+its own replica (no data-path collective yet).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "CPR-GMRES solve time & iters, SPE10-shape 3.28M DOF; smoother/SpMV HBM GB/s"
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _grid(s):
+    return tuple(int(v) for v in s.split(","))
+
+
+def _bytes_spmv(nb, nnzb):
+    return nnzb * (72 + 4) + (nb + 1) * 4 + 2 * (3 * nb) * 8
+
+
+def _bytes_sweep(n, nnz):
+    return (nnz - n) * 12 + n * 36
+
+
+def _bytes_bilu(nb, n_off_l, n_off_u):
+    return (n_off_l + n_off_u) * 76 + nb * 72 + 2 * (nb + 1) * 4 + 4 * 3 * nb * 8
+
+
+def _time_op(fn, reps, torch):
+    st = torch.cuda.current_stream()
+    for _ in range(2):
+        fn()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(reps):
+        fn()
+    e1.record(st)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps * 1e3   # microseconds
+
+
+def run_ours(args):
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2201_01970_b200 as P
+    from paper_2201_01970_b200 import _native as N
+    from paper_2201_01970_b200 import device as D
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    nx, ny, nz = args.grid
+    t0 = time.perf_counter()
+    (A, b), = P.generate_blackoil_like_sequence(nx, ny, nz, 1, 0.01, 0).systems
+    t_gen = time.perf_counter() - t0
+    cfg = P.SolverConfig(theta=0.0, theta_amg=0.0, cycle=args.cycle)
+    t0 = time.perf_counter()
+    B = P.build_cpr(A, cfg)
+    Bd = B.device()
+    M = D.device_matrix(A)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t0
+    n = b.shape[0]
+    bd = torch.from_numpy(b).cuda()
+    params = cfg.gmres_params()
+    lib = N.lib()
+    launches = {"n": 0}
+
+    def solve():
+        return P.gmres_solve(A, bd, None, B, params)
+
+    for _ in range(args.warmup):
+        res = solve()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    st = torch.cuda.current_stream()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        e0.record(st)
+        for _ in range(args.steps):
+            res = solve()
+        e1.record(st)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    if ws > 1:
+        tt = torch.tensor([ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+        dist.barrier()
+    x_dev = res.x
+    xs = P.problems.manufactured_solution(nx * ny * nz)
+    x_err = float(np.linalg.norm(x_dev.cpu().numpy() - xs) / np.linalg.norm(xs))
+
+    # e2e: public API from pinned host buffers (H2D of b, D2H of x inside)
+    b_pin = torch.from_numpy(b).pin_memory()
+    P.gmres_solve(A, b_pin, None, B, params)
+    torch.cuda.synchronize()
+    te = []
+    for _ in range(max(1, min(args.steps, 3))):
+        t0 = time.perf_counter()
+        r2 = P.gmres_solve(A, b_pin, None, B, params)
+        _ = r2.x.numpy()
+        te.append(time.perf_counter() - t0)
+    e2e_ms = float(np.median(te) * 1e3)
+    small = sum((j + 2) * 8 + 16 for j in range(res.inner)) + 8 * (3 + 2 * res.outer)
+
+    # per-kernel timing on the launching stream (CUDA events), algorithmic bytes
+    peak, peak_kind = _peaks()
+    nb, nnzb = A.nrows, A.nnz
+    w = D.empty(n)
+    z = D.empty(n)
+    lvl0 = Bd.amg.levels[0]
+    A0 = B.pressure_solver.levels[0].A
+    kern = {}
+    reps = 20
+    us = _time_op(lambda: lib.cprb_spmv(M.desc_ref(), 3, D.ptr(bd), D.ptr(w), None, D.stream()), reps, torch)
+    kern["bsr_spmv"] = (us, _bytes_spmv(nb, nnzb))
+    bp = D.empty(A0.nrows)
+    xp = D.zeros(A0.nrows)
+    bp.copy_(torch.from_numpy(np.ascontiguousarray(b[0::3])).cuda())
+    us = _time_op(lambda: lib.cprb_pgs_scm_pass(C.byref(lvl0.desc), D.ptr(bp), D.ptr(xp), 1, 0,
+                                                D.stream()), reps, torch)
+    kern["pgs_scm_sweep_l0"] = (us, _bytes_sweep(A0.nrows, A0.nnz))
+    Fl = B.relaxation
+    n_off_l = Fl.L.nnz - nb
+    n_off_u = Fl.U.nnz - nb
+    us = _time_op(lambda: Bd.bilu.apply(bd, z), reps, torch)
+    kern["bilu_apply"] = (us, _bytes_bilu(nb, n_off_l, n_off_u))
+    zp = D.empty(nb)
+    us = _time_op(lambda: Bd.amg.vcycle(bd, zp), reps, torch)
+    lv = B.pressure_solver.levels
+    vbytes = sum(2 * _bytes_sweep(l.A.nrows, l.A.nnz) + l.A.nnz * 12 + l.A.nrows * 28
+                 for l in lv[:-1])
+    kern["amg_vcycle"] = (us, vbytes)
+    us = _time_op(lambda: Bd.apply(bd, z), reps, torch)
+    kern["cpr_apply"] = (us, None)
+    kernels = {}
+    for k, (us_, byt) in kern.items():
+        d = {"us": round(us_, 2)}
+        if byt:
+            gbs = byt / (us_ * 1e-6) / 1e9
+            d.update({"bytes": int(byt), "GB/s": round(gbs, 1), "frac": round(gbs / peak, 4)})
+        kernels[k] = d
+    # dominant kernel over one solve: count per-solve invocations
+    napply = res.inner + res.outer
+    share = {"bilu_apply": kern["bilu_apply"][0] * napply,
+             "amg_vcycle": kern["amg_vcycle"][0] * napply,
+             "bsr_spmv": kern["bsr_spmv"][0] * (2 * res.inner + 2 * res.outer + napply)}
+    dom = max(share, key=share.get)
+    dus, dbytes = kern[dom]
+    achieved = dbytes / (dus * 1e-6) / 1e9
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                "traffic": None, "share_of_step": round(share[dom] * 1e-3 / ms, 3)}
+
+    out = {
+        "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generator restated bitwise: seed 0, drift 0.01)",
+        "config": {"workload": f"SPE10-shaped {nx}x{ny}x{nz} three-phase BSR3 CPR-GMRES solve "
+                               f"(config 3), SolverConfig(theta=0, theta_amg=0, cycle='{args.cycle}')",
+                   "dof": n, "nnz_blocks": nnzb, "levels": len(lv),
+                   "parallelism": "replicas" if ws > 1 else "single-gpu",
+                   "l2": "working set > 1 GB exceeds 126 MB L2; no flush"},
+        "iters": {"outer": res.outer, "inner": res.inner, "rel_residual": res.rel_residual,
+                  "x_err_vs_manufactured": x_err},
+        "e2e": {"value": round(e2e_ms, 4), "unit": "ms", "h2d_bytes_per_step": int(8 * n),
+                "d2h_bytes_per_step": int(8 * n + small)},
+        "roofline": roofline, "kernels": kernels,
+        "setup_s": round(t_setup, 2), "generate_s": round(t_gen, 2),
+        "gpu_launches": None, "clocks": clk.summary(),
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(A, b, args, sample=True)
+    if rank == 0:
+        print(json.dumps(out))
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def cpu_baseline(A, b, args, sample=True):
+    """The oracle's CPR-GMRES solve on the host (1 thread: the reference's
+    GIL-bound path), on the same system and config.  Setup comes from the
+    oracle's own restatement of the reference's setup."""
+    from oracle import cprkit_oracle as orc
+    Ao = orc.Bsr(3, A.nrows, A.ncols, A.row_ptr, A.col_idx, A.values)
+    cfg = orc.SolverConfig(theta=0.0, theta_amg=0.0, cycle=args.cycle)
+    t0 = time.perf_counter()
+    B = orc.build_cpr(Ao, cfg)
+    t_setup = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    res = orc.gmres_solve(Ao, b, None, B, cfg.m, cfg.max_restarts, cfg.tol)
+    t_solve = time.perf_counter() - t0
+    return {"value": round(t_solve * 1e3, 1), "unit": "ms", "cores": 1, "kind": "port",
+            "sample": f"one full CPR-GMRES solve of the same {A.nrows * 3}-DOF system "
+                      f"(outer={res.outer}, inner={res.inner}); oracle setup {t_setup:.1f} s "
+                      "untimed; numpy/OpenBLAS single thread",
+            "host_cpus": os.cpu_count()}
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    sys.path.insert(0, str(ROOT))
+    from oracle import cprkit_oracle as orc
+    nx, ny, nz = args.grid
+    (A, b), = orc.generate_blackoil_like_sequence(nx, ny, nz, 1, 0.01, 0)
+    cfg = orc.SolverConfig(theta=0.0, theta_amg=0.0, cycle=args.cycle)
+    t0 = time.perf_counter()
+    B = orc.build_cpr(A, cfg)
+    t_setup = time.perf_counter() - t0
+    times = []
+    res = None
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        res = orc.gmres_solve(A, b, None, B, cfg.m, cfg.max_restarts, cfg.tol)
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    ms = float(np.mean(times) * 1e3)
+    out = {"impl": "reference", "metric": METRIC, "value": round(ms, 2), "unit": "ms",
+           "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 2),
+           "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (reference generator, seed 0, drift 0.01)",
+           "config": {"workload": f"SPE10-shaped {nx}x{ny}x{nz} three-phase BSR3 CPR-GMRES solve "
+                                  f"(config 3), SolverConfig(theta=0, theta_amg=0, cycle='{args.cycle}')",
+                      "dof": int(b.shape[0])},
+           "iters": {"outer": res.outer, "inner": res.inner, "rel_residual": res.rel_residual},
+           "cpu_baseline": {"value": round(ms, 2), "unit": "ms", "cores": 1, "kind": "port",
+                            "sample": "full solves of the config-3 system by the oracle port "
+                                      f"(setup {t_setup:.1f} s untimed)",
+                            "host_cpus": os.cpu_count()},
+           "e2e": {"value": round(ms, 2), "unit": "ms", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--grid", type=_grid, default=(60, 220, 85))
+    ap.add_argument("--cycle", default="v", choices=["v", "k"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,224 @@
+/*
+ * cpr_b200.h — C ABI of the B200-native CPR-GMRES SOLVE path.
+ *
+ * The reference (cprkit, pure Python) has no FFI: its boundary is the Python
+ * API.  This header is the C-ABI the Python drop-in
+ * (paper_2201_01970_b200) binds through ctypes; each entry point names the
+ * reference function it replaces (src/X.py:N = cprkit/X.py line N).
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  "dev" pointers are CUDA device memory
+ *    (owned by the caller, e.g. torch tensors); everything else is host.
+ *  - `stream` is a cudaStream_t passed as void*; all device calls are
+ *    stream-ordered and asynchronous unless stated.
+ *  - Return value: CPRB_OK or an error code; cprb_last_error() gives the
+ *    message (thread-local).  The Python layer maps codes to the reference's
+ *    exception types.
+ *  - Index types: setup uses int64 (the reference's index dtype); device
+ *    layouts use int32 (max nnz at the 26.9M-DOF config is 6.3e7 blocks).
+ */
+#ifndef CPR_B200_H
+#define CPR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  CPRB_OK = 0,
+  CPRB_EINVAL = 1,     /* ValueError            (e.g. dimension mismatch) */
+  CPRB_ENONFINITE = 2, /* FloatingPointError    (src/cpr.py:248,274,307) */
+  CPRB_ESINGULAR = 3,  /* numpy.linalg.LinAlgError (src/ilu.py:140,147; src/smoothers.py:89) */
+  CPRB_EDEVICE = 4,    /* RuntimeError: CUDA failure */
+  CPRB_ERUNTIME = 5,   /* RuntimeError (src/amg.py:172) */
+  CPRB_EUNSUPPORTED = 6
+};
+
+const char* cprb_last_error(void);
+int cprb_version(void);
+
+/* ======================= host setup (SETUP phase) ======================= */
+
+/* src/coloring.py:79-114  S(A,theta): S_ij iff i!=j and |a_ij| > theta*sum_k|a_ik|
+ * (row sum in numpy reduceat order).  s_ptr[n+1], s_cols[capacity nnz]. */
+int cprb_strong_connections(int64_t n, const int64_t* ptr, const int64_t* cols,
+                            const double* vals, double theta, int64_t* s_ptr,
+                            int64_t* s_cols);
+
+/* src/coloring.py:238-256 (+ vertices_splitting :171-235)  greedy colour
+ * groups on S ∪ S^T.  perm[n] = concatenated ascending groups;
+ * group_sizes[capacity n]; *ncolors = number of groups. */
+int cprb_vertices_grouping(int64_t n, const int64_t* s_ptr, const int64_t* s_cols,
+                           int64_t* perm, int64_t* group_sizes, int64_t* ncolors);
+
+/* src/amg.py:89-119  greedy pairwise aggregation (NPAIR). agg[n], *n_agg. */
+int cprb_pairwise_aggregate(int64_t n, const int64_t* ptr, const int64_t* cols,
+                            const double* vals, double theta_amg, int64_t* agg,
+                            int64_t* n_agg);
+
+/* src/amg.py:127-132  Galerkin A_c = P^T A P for piecewise-constant P,
+ * duplicate sums in stable-lexsort + reduceat order.  Outputs have capacity
+ * nnz(A); c_ptr[n_agg+1]; *c_nnz. */
+int cprb_galerkin(int64_t n, const int64_t* ptr, const int64_t* cols, const double* vals,
+                  const int64_t* agg, int64_t n_agg, int64_t* c_ptr, int64_t* c_cols,
+                  double* c_vals, int64_t* c_nnz);
+
+/* src/amg.py:135-140 */
+int cprb_is_symmetric(int64_t n, const int64_t* ptr, const int64_t* cols, const double* vals,
+                      double tol, int32_t* out);
+
+/* src/ilu.py:150-193  BILU(0), IKJ on the pattern; `vals` (nnz*b*b) is
+ * overwritten with the factors, uinv[n*b*b] = inverted pivots (Gauss-Jordan,
+ * src/sparse.py:372-396).  Perturbed pivots (src/ilu.py:134-147) are listed in
+ * perturbed[capacity n]; *n_perturbed.  CPRB_ESINGULAR names the row. */
+int cprb_bilu0_factorize(int64_t n, int32_t b, const int64_t* ptr, const int64_t* cols,
+                         double* vals, double* uinv, int64_t* perturbed,
+                         int64_t* n_perturbed);
+
+/* src/ilu.py:38-59  level[i] (1-based) of a triangular pattern; *nlevels. */
+int cprb_level_schedule(int64_t n, const int64_t* ptr, const int64_t* cols,
+                        int64_t* level, int64_t* nlevels);
+
+/* coarsest level (replaces scipy lu_factor/lu_solve, src/amg.py:170-173,
+ * :248-249): dense inverse via LU with partial pivoting; a: n*n row-major. */
+int cprb_dense_inverse(int64_t n, const double* a, double* inv);
+
+/* src/sparse.py:372-396 batched 3x3/bxb Gauss-Jordan inverse (bitwise). */
+int cprb_invert_small_blocks(int64_t m, int32_t b, const double* blocks, double* out);
+
+/* ===================== device layouts (SOLVE phase) ===================== */
+
+/* SELL-32 sliced-ELL storage.  Slice s owns 32 lanes; lane l of slice s maps
+ * to row lane_row[s*32+l] (-1 = padding).  Entry m of that lane is at
+ * e = slice_ptr[s] + m*32 + l:  cols[e];  scalar value vals[e];  b x b block
+ * value (r,c) at vals[(slice_ptr[s] + m*32)*b*b + (r*b+c)*32 + l].
+ * Entries of a row keep the reference's summation order. */
+typedef struct cprb_sell {
+  int32_t nslices;
+  int32_t nrows;
+  const int64_t* slice_ptr;   /* dev, nslices+1 (entry units) */
+  const int32_t* lane_row;    /* dev, nslices*32 */
+  const int32_t* lane_len;    /* dev, nslices*32 */
+  const int32_t* lane_len_lo; /* dev|NULL: entries with col < colour start */
+  const int32_t* cols;        /* dev */
+  const double* vals;         /* dev */
+  const int32_t* agg_out;     /* dev|NULL: restriction output index per lane pair */
+} cprb_sell;
+
+/* One smoothed AMG level (src/amg.py:68-74 AmgLevel), in colour-permuted
+ * order.  HOST arrays: colour bounds. */
+typedef struct cprb_amg_level {
+  int32_t n;
+  int32_t ncolors;
+  const int32_t* color_slices; /* host, ncolors+1 (slice bounds in `smoother`) */
+  const int32_t* color_rows;   /* host, ncolors+1 (row bounds, permuted)        */
+  const uint8_t* color_snapshot; /* host, ncolors: 1 = intra-colour couplings  */
+  cprb_sell smoother;          /* off-diagonals, ascending permuted columns     */
+  const double* diag;          /* dev, n */
+  cprb_sell restrict_op;       /* rows grouped by aggregate (lane pairs), original column order */
+  const int32_t* aggp;         /* dev, n: coarse (permuted) index of each row   */
+  double* b;                   /* dev work, n */
+  double* x;                   /* dev work, n */
+  double* tmp;                 /* dev work, n (snapshot sweeps) */
+} cprb_amg_level;
+
+typedef struct cprb_amg {
+  int32_t nlevels;                  /* total, including the coarsest */
+  const cprb_amg_level* levels;     /* host array, nlevels-1 entries  */
+  int32_t n_coarse;
+  const double* coarse_inv;         /* dev, n_coarse^2 row-major */
+  double* coarse_b;                 /* dev work */
+  double* coarse_x;                 /* dev work */
+  const int32_t* perm0;             /* dev, n0: level-0 permuted row -> fine index */
+  int32_t in_stride;                /* residual stride of the level-0 input (b of BSR, 1 scalar) */
+  int32_t cycle;                    /* 0 = V, 1 = K */
+  int32_t use_fcg;                  /* K-cycle Krylov flavour */
+  double* kwork;                    /* dev work for the K-cycle (see engine) */
+  int64_t kwork_len;
+} cprb_amg;
+
+typedef struct cprb_bilu {
+  int32_t n;                   /* block rows */
+  int32_t b;                   /* block size (1 or 3) */
+  cprb_sell L;                 /* strict lower blocks; lanes in L-level order */
+  cprb_sell U;                 /* strict upper blocks; lanes in U-level order */
+  const double* uinv;          /* dev, U lane layout: [(s*b*b + e)*32 + l] */
+  int32_t* tickets;            /* dev, 2 ints (dynamic warp ordering) */
+} cprb_bilu;
+
+typedef struct cprb_cpr {
+  int32_t nb;                  /* block rows */
+  int32_t b;                   /* block size */
+  cprb_sell A;                 /* build-time matrix (stage-2 residual) */
+  cprb_amg amg;
+  cprb_bilu bilu;
+  double* zp;                  /* dev work, nb: pressure correction, natural order */
+  double* r2;                  /* dev work, nb*b */
+  double* zl;                  /* dev work, nb*b (L-solve, sentinel polled) */
+  double* y;                   /* dev work, nb*b (U-solve, sentinel polled) */
+} cprb_cpr;
+
+/* ============================ device kernels ============================ */
+
+/* src/sparse.py:335-351  y = A x (BSR via the expanded-row order).  flag
+ * (dev|NULL) is set to 1 when any y is non-finite. */
+int cprb_spmv(const cprb_sell* A, int32_t b, const double* x, double* y, int32_t* flag,
+              void* stream);
+/* r = rhs - A x  (src/cpr.py:246, :306) */
+int cprb_residual(const cprb_sell* A, int32_t b, const double* rhs, const double* x,
+                  double* r, int32_t* flag, void* stream);
+
+/* src/smoothers.py:273-318  one PGS-SCM pass over a level (permuted vectors).
+ * direction 0 forward / 1 backward; zero_guess: x is treated as 0. */
+int cprb_pgs_scm_pass(const cprb_amg_level* lvl, const double* b, double* x, int32_t direction,
+                      int32_t zero_guess, void* stream);
+
+/* src/amg.py:228-267  z = amg_cycle(h, r); r strided by h->in_stride. */
+int cprb_amg_cycle(const cprb_amg* h, const double* r, double* z, void* stream);
+
+/* K-cycle building blocks (the K-cycle recursion, src/amg.py:177-225,
+ * :256-263, is driven by the host layer with these device steps). */
+int cprb_coarse_solve(const cprb_amg* h, const double* b, double* x, void* stream);
+int cprb_resid_restrict(const cprb_amg_level* lvl, const double* b, const double* x, double* bc,
+                        void* stream);
+int cprb_prolong(const cprb_amg_level* lvl, const double* xc, double* x, void* stream);
+
+/* src/ilu.py:196-223  z = U^{-1} L^{-1} r (level-ordered, sync-free). */
+int cprb_bilu_apply(const cprb_bilu* F, const double* r, double* z, double* work_l,
+                    void* stream);
+
+/* src/cpr.py:178-186  z = B r (V-cycle pressure stage). */
+int cprb_cpr_apply(const cprb_cpr* P, const double* r, double* z, void* stream);
+/* src/cpr.py:184-186  second half given zp already in P->zp. */
+int cprb_cpr_finish(const cprb_cpr* P, const double* r, double* z, void* stream);
+
+/* Deterministic reductions (fixed block partition + fixed tree).
+ * partials: dev, >= CPRB_RED_BLOCKS doubles; ticket: dev int (zeroed once). */
+#define CPRB_RED_BLOCKS 1184
+int cprb_dot(int64_t n, const double* x, const double* y, double* out, double* partials,
+             int32_t* ticket, void* stream);
+
+/* src/cpr.py:276-284  Arnoldi MGS for column j: for i<=j: H[i]=(w,V_i),
+ * w -= H[i] V_i; H[j+1] = ||w||; V_{j+1} = w / H[j+1] (if nonzero).
+ * V: (j+2) rows of length n (row stride ldv); w is V_{j+1} (in place). */
+int cprb_arnoldi_mgs(int64_t n, int32_t j, double* V, int64_t ldv, double* Hcol,
+                     double* partials, int32_t* ticket, void* stream);
+
+/* u = sum_i y[i] V_i  (src/cpr.py:304), y: dev, k entries */
+int cprb_gemv_t(int64_t n, int32_t k, const double* V, int64_t ldv, const double* y, double* u,
+                void* stream);
+/* out = x + s (elementwise, src/cpr.py:305) */
+int cprb_add(int64_t n, const double* x, const double* s, double* out, void* stream);
+/* out = alpha * x + y  (src/sparse.py:354-358; also the FCG updates of src/amg.py:188-194) */
+int cprb_axpy(int64_t n, double alpha, const double* x, const double* y, double* out, void* stream);
+/* out = x / h (host scalar; src/amg.py:204 rhs / beta) */
+int cprb_div_host(int64_t n, const double* x, double h, double* out, void* stream);
+/* out = x / (*h_dev)  (src/cpr.py:262 V[0] = r / beta) */
+int cprb_div_scalar(int64_t n, const double* x, const double* h_dev, double* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CPR_B200_H */

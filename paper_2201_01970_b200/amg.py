@@ -1,0 +1,457 @@
+"""Unsmoothed-aggregation AMG for the pressure operator (drop-in for
+cprkit.amg).
+
+SETUP (host C++, bit-exact structure): NPAIR aggregation, colour grouping,
+Galerkin products, stall rule and level cap exactly as src/amg.py:143-174;
+the coarsest level gets a dense inverse (replacing scipy's lu_factor /
+lu_solve; values agree to rounding).
+SOLVE (device): the V-cycle is one C-ABI call that launches the colour sweeps,
+fused residual + restriction, prolongation and coarse solve
+(csrc/amg.cu).  The K-cycle (src/amg.py:177-225) is driven from here: the
+recursion and the Krylov scalars stay on the host, every vector operation
+runs on the device.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _native as N
+from . import device as D
+from .coloring import ColorPartition, strong_connections, vertices_grouping
+from .smoothers import PgsScmSmoother, SmootherSpec, make_smoother
+from .sparse import CsrMatrix
+
+__all__ = ["AggregationMap", "AmgParams", "AmgLevel", "AmgHierarchy", "pairwise_aggregate",
+           "build_hierarchy", "amg_cycle", "hierarchy_summary"]
+
+
+@dataclass
+class AggregationMap:
+    aggregate_of: np.ndarray
+    n_aggregates: int
+
+
+@dataclass
+class AmgParams:
+    """src/amg.py:41-66 (same fields, defaults and validation)."""
+
+    coarsest_size: int = 200
+    max_levels: int = 25
+    theta_amg: float = 0.08
+    smoother_theta: float = 0.0
+    smoother_kind: str = "pgs-scm"
+    pre_sweeps: int = 1
+    post_sweeps: int = 1
+    cycle: str = "k"
+    krylov: str = "auto"
+
+    def __post_init__(self):
+        if self.cycle not in ("v", "k"):
+            raise ValueError(f"cycle must be 'v' or 'k', got {self.cycle!r}")
+        if self.krylov not in ("auto", "fcg", "fgmres"):
+            raise ValueError(f"unknown krylov selector {self.krylov!r}")
+
+
+@dataclass
+class AmgLevel:
+    A: CsrMatrix
+    partition: Optional[ColorPartition]
+    smoother: object
+    P: Optional[CsrMatrix] = None
+    aggregates: Optional[np.ndarray] = None
+
+
+@dataclass
+class AmgHierarchy:
+    levels: list
+    coarsest_lu: tuple          # ("inverse", dense inverse of the coarsest operator)
+    params: AmgParams
+    symmetric: bool = False
+    _dev: object = None
+
+    @property
+    def fine_size(self) -> int:
+        return self.levels[0].A.nrows
+
+    def device(self, in_stride: int = 1) -> "DeviceAmg":
+        if self._dev is None or self._dev.in_stride != in_stride:
+            self._dev = DeviceAmg(self, in_stride)
+        return self._dev
+
+
+def _csr_arrays(A):
+    return (np.ascontiguousarray(A.row_ptr, dtype=np.int64),
+            np.ascontiguousarray(A.col_idx, dtype=np.int64),
+            np.ascontiguousarray(A.values, dtype=np.float64))
+
+
+def pairwise_aggregate(A, theta_amg: float) -> AggregationMap:
+    """Greedy pairwise matching (src/amg.py:89-119), host C++."""
+    if A.nrows != A.ncols:
+        raise ValueError("aggregation needs a square matrix")
+    if not 0.0 <= theta_amg <= 1.0:
+        raise ValueError(f"theta must lie in [0, 1], got {theta_amg}")
+    p, c, v = _csr_arrays(A)
+    agg = np.zeros(A.nrows, dtype=np.int64)
+    na = np.zeros(1, dtype=np.int64)
+    N.check(N.lib().cprb_pairwise_aggregate(A.nrows, N.p64(p), N.p64(c if c.size else np.zeros(1, np.int64)),
+                                            N.pf64(v if v.size else np.zeros(1)), float(theta_amg),
+                                            N.p64(agg), N.p64(na)))
+    return AggregationMap(agg, int(na[0]))
+
+
+def _prolongation(agg: AggregationMap, n: int) -> CsrMatrix:
+    return CsrMatrix(n, agg.n_aggregates, np.arange(n + 1, dtype=np.int64),
+                     agg.aggregate_of.copy(), np.ones(n))
+
+
+def _galerkin(A, agg: AggregationMap) -> CsrMatrix:
+    """A_c[I, J] = sum of A_ij over aggregate pairs (src/amg.py:127-132), host C++."""
+    p, c, v = _csr_arrays(A)
+    cap = max(c.shape[0], 1)
+    cp = np.zeros(agg.n_aggregates + 1, dtype=np.int64)
+    cc = np.zeros(cap, dtype=np.int64)
+    cv = np.zeros(cap)
+    nnz = np.zeros(1, dtype=np.int64)
+    a = np.ascontiguousarray(agg.aggregate_of, dtype=np.int64)
+    N.check(N.lib().cprb_galerkin(A.nrows, N.p64(p), N.p64(c if c.size else np.zeros(1, np.int64)),
+                                  N.pf64(v if v.size else np.zeros(1)), N.p64(a), agg.n_aggregates,
+                                  N.p64(cp), N.p64(cc), N.pf64(cv), N.p64(nnz)))
+    k = int(nnz[0])
+    return CsrMatrix(agg.n_aggregates, agg.n_aggregates, cp, cc[:k].copy(), cv[:k].copy())
+
+
+def _is_symmetric(A, tol: float = 1e-12) -> bool:
+    p, c, v = _csr_arrays(A)
+    out = np.zeros(1, dtype=np.int32)
+    N.check(N.lib().cprb_is_symmetric(A.nrows, N.p64(p), N.p64(c if c.size else np.zeros(1, np.int64)),
+                                      N.pf64(v if v.size else np.zeros(1)), tol, N.p32(out)))
+    return bool(out[0])
+
+
+def _dense_inverse(A) -> np.ndarray:
+    n = A.nrows
+    dense = np.ascontiguousarray(A.to_dense())
+    inv = np.zeros((n, n))
+    N.check(N.lib().cprb_dense_inverse(n, N.pf64(dense), N.pf64(inv)))
+    return inv
+
+
+def build_hierarchy(A_p, params: AmgParams | None = None) -> AmgHierarchy:
+    """src/amg.py:143-174: aggregate / project until the coarsest target, the
+    level cap or a coarsening stall (n_agg > 0.9 n)."""
+    params = params or AmgParams()
+    if A_p.nrows != A_p.ncols:
+        raise ValueError("hierarchy needs a square matrix")
+    if not isinstance(A_p, CsrMatrix):
+        A_p = CsrMatrix(A_p.nrows, A_p.ncols, A_p.row_ptr, A_p.col_idx, A_p.values)
+    levels = []
+    A_l = A_p
+    sym = _is_symmetric(A_p)
+    while True:
+        if A_l.nrows <= params.coarsest_size or len(levels) + 1 >= params.max_levels:
+            levels.append(AmgLevel(A_l, None, None))
+            break
+        agg = pairwise_aggregate(A_l, params.theta_amg)
+        if agg.n_aggregates > 0.9 * A_l.nrows:
+            levels.append(AmgLevel(A_l, None, None))
+            break
+        partition = vertices_grouping(strong_connections(A_l, params.smoother_theta))
+        spec = SmootherSpec(kind=params.smoother_kind,
+                            partition=partition if params.smoother_kind == "pgs-scm" else None)
+        smoother = make_smoother(A_l, spec)
+        levels.append(AmgLevel(A_l, partition, smoother, P=_prolongation(agg, A_l.nrows),
+                               aggregates=agg.aggregate_of))
+        A_l = _galerkin(A_l, agg)
+    try:
+        inv = _dense_inverse(levels[-1].A)
+    except RuntimeError as exc:
+        raise RuntimeError(str(exc)) from exc
+    return AmgHierarchy(levels, ("inverse", inv), params, symmetric=sym)
+
+
+def hierarchy_summary(h: AmgHierarchy) -> dict:
+    """src/amg.py:270-285."""
+    sizes = [lvl.A.nrows for lvl in h.levels]
+    nnzs = [lvl.A.nnz for lvl in h.levels]
+    return {
+        "levels": len(h.levels),
+        "sizes": sizes,
+        "nnz": nnzs,
+        "colors": [lvl.partition.c if lvl.partition is not None else None for lvl in h.levels],
+        "operator_complexity": float(sum(nnzs)) / max(nnzs[0], 1),
+        "grid_complexity": float(sum(sizes)) / max(sizes[0], 1),
+        "cycle": h.params.cycle,
+        "coarsest_size": sizes[-1],
+        "symmetric": h.symmetric,
+    }
+
+
+# ----------------------------------------------------------------------------
+# device plan
+# ----------------------------------------------------------------------------
+
+
+def _restriction_sell(A, agg: np.ndarray, n_agg: int, inv_l: np.ndarray, inv_c: np.ndarray):
+    """Rows grouped by aggregate: lane 2I = lower member, lane 2I+1 = upper member
+    (or a dummy), entries in the ORIGINAL column order mapped to permuted
+    columns; agg_out[I] = permuted coarse index."""
+    n = A.nrows
+    order = np.argsort(agg, kind="stable")          # members ascending inside each aggregate
+    counts = np.bincount(agg, minlength=n_agg)
+    first = np.zeros(n_agg + 1, dtype=np.int64)
+    np.cumsum(counts, out=first[1:])
+    lane_orig = np.full(2 * n_agg, -1, dtype=np.int64)
+    lane_orig[0::2] = order[first[:-1]]
+    two = counts == 2
+    lane_orig[1::2][two] = order[first[:-1][two] + 1]
+    lane_orig = D.pad_lanes(lane_orig)
+    L = lane_orig.shape[0]
+    real = lane_orig >= 0
+    ptr = np.asarray(A.row_ptr, dtype=np.int64)
+    lens = np.zeros(L, dtype=np.int64)
+    lens[real] = (ptr[1:] - ptr[:-1])[lane_orig[real]]
+    lane_ptr = np.zeros(L + 1, dtype=np.int64)
+    np.cumsum(lens, out=lane_ptr[1:])
+    nnz = int(lane_ptr[-1])
+    lane_of = np.repeat(np.arange(L, dtype=np.int64), lens)
+    src = ptr[lane_orig[lane_of]] + (np.arange(nnz, dtype=np.int64) - lane_ptr[lane_of])
+    cols = inv_l[np.asarray(A.col_idx, dtype=np.int64)[src]]
+    vals = np.asarray(A.values, dtype=np.float64)[src]
+    lane_row = np.where(real, inv_l[np.maximum(lane_orig, 0)], -1).astype(np.int32)
+    agg_out = np.full(L // 2, -1, dtype=np.int32)
+    agg_out[:n_agg] = inv_c[np.arange(n_agg)]
+    return D.pack_sell(lane_row, lane_ptr, cols, vals, 1, n, agg_out=agg_out)
+
+
+def _permuted_rows_sell(A, perm: np.ndarray, inv: np.ndarray):
+    """A_l with rows in permuted order, each row in ORIGINAL column order
+    (cols mapped to permuted indices): spmv on permuted vectors with the
+    reference's row sums (K-cycle Krylov steps)."""
+    n = A.nrows
+    ptr = np.asarray(A.row_ptr, dtype=np.int64)
+    lane_orig = D.pad_lanes(perm.astype(np.int64))
+    L = lane_orig.shape[0]
+    real = lane_orig >= 0
+    lens = np.zeros(L, dtype=np.int64)
+    lens[real] = np.diff(ptr)[lane_orig[real]]
+    lane_ptr = np.zeros(L + 1, dtype=np.int64)
+    np.cumsum(lens, out=lane_ptr[1:])
+    nnz = int(lane_ptr[-1])
+    lane_of = np.repeat(np.arange(L, dtype=np.int64), lens)
+    src = ptr[lane_orig[lane_of]] + (np.arange(nnz, dtype=np.int64) - lane_ptr[lane_of])
+    cols = inv[np.asarray(A.col_idx, dtype=np.int64)[src]]
+    vals = np.asarray(A.values, dtype=np.float64)[src]
+    lane_row = np.where(real, np.arange(L), -1).astype(np.int32)
+    return D.pack_sell(lane_row, lane_ptr, cols, vals, 1, n)
+
+
+class DeviceAmg:
+    """Device-resident hierarchy: per level the colour-permuted smoother, the
+    fused residual/restriction operator, the prolongation map and work
+    vectors; the coarsest dense inverse."""
+
+    def __init__(self, h: AmgHierarchy, in_stride: int = 1):
+        D.require_cuda()
+        self.h = h
+        self.in_stride = int(in_stride)
+        L = len(h.levels)
+        self.nlevels = L
+        perms, invs = [], []
+        for lvl in h.levels:
+            n = lvl.A.nrows
+            if lvl.smoother is not None:
+                p = lvl.smoother.perm.astype(np.int64)
+            else:
+                p = np.arange(n, dtype=np.int64)
+            inv = np.empty(n, dtype=np.int64)
+            inv[p] = np.arange(n, dtype=np.int64)
+            perms.append(p)
+            invs.append(inv)
+        self.perms, self.invs = perms, invs
+        self.levels = []
+        self.restrict = []
+        self.aggp = []
+        self.kspmv = []
+        for l in range(L - 1):
+            lvl = h.levels[l]
+            if not isinstance(lvl.smoother, PgsScmSmoother):
+                raise NotImplementedError("device AMG levels use the PGS-SCM smoother")
+            dl = lvl.smoother.device()
+            na = h.levels[l + 1].A.nrows
+            R = D.SellDev(_restriction_sell(lvl.A, lvl.aggregates, na, invs[l], invs[l + 1]))
+            aggp = D.upload(invs[l + 1][lvl.aggregates[perms[l]]].astype(np.int32))
+            dl.desc.restrict_op = R.desc
+            dl.desc.aggp = D.ptr(aggp)
+            self.levels.append(dl)
+            self.restrict.append(R)
+            self.aggp.append(aggp)
+            self.kspmv.append(None)
+        self.level_arr = (N.AmgLevel * max(L - 1, 1))()
+        for l, dl in enumerate(self.levels):
+            self.level_arr[l] = dl.desc
+        inv = h.coarsest_lu[1]
+        self.n_coarse = inv.shape[0]
+        self.coarse_inv = D.upload(np.ascontiguousarray(inv).reshape(-1))
+        self.coarse_b = D.empty(self.n_coarse)
+        self.coarse_x = D.empty(self.n_coarse)
+        self.perm0 = D.upload(perms[0].astype(np.int32))
+        self.desc = N.Amg()
+        self.desc.nlevels = L
+        self.desc.levels = self.level_arr
+        self.desc.n_coarse = self.n_coarse
+        self.desc.coarse_inv = D.ptr(self.coarse_inv)
+        self.desc.coarse_b = D.ptr(self.coarse_b)
+        self.desc.coarse_x = D.ptr(self.coarse_x)
+        self.desc.perm0 = D.ptr(self.perm0)
+        self.desc.in_stride = self.in_stride
+        self.desc.cycle = 0
+        self.desc.use_fcg = 1 if (h.params.krylov == "fcg" or
+                                  (h.params.krylov == "auto" and h.symmetric)) else 0
+
+    # -- V-cycle: one native call ------------------------------------------------
+    def vcycle(self, r, z):
+        N.check(N.lib().cprb_amg_cycle(C.byref(self.desc), D.ptr(r), D.ptr(z), D.stream()))
+
+    # -- K-cycle: host recursion over device steps (src/amg.py:245-267) ----------
+    def _kspmv(self, l):
+        if self.kspmv[l] is None:
+            lvl = self.h.levels[l]
+            self.kspmv[l] = D.SellDev(_permuted_rows_sell(lvl.A, self.perms[l], self.invs[l]))
+        return self.kspmv[l]
+
+    def _spmv_level(self, l, x):
+        y = D.empty(x.shape[0])
+        N.check(N.lib().cprb_spmv(C.byref(self._kspmv(l).desc), 1, D.ptr(x), D.ptr(y), None,
+                                  D.stream()))
+        return y
+
+    def _cycle_at(self, l, b, use_fcg, cycle):
+        L = self.nlevels
+        if l == L - 1:
+            x = D.empty(self.n_coarse)
+            N.check(N.lib().cprb_coarse_solve(C.byref(self.desc), D.ptr(b), D.ptr(x), D.stream()))
+            return x
+        dl = self.levels[l]
+        p = self.h.params
+        x = D.empty(b.shape[0])
+        lib, st = N.lib(), D.stream()
+        for s in range(p.pre_sweeps):
+            N.check(lib.cprb_pgs_scm_pass(C.byref(dl.desc), D.ptr(b), D.ptr(x), 0,
+                                          1 if s == 0 else 0, st))
+        nc = self.h.levels[l + 1].A.nrows
+        rc = D.empty(nc)
+        N.check(lib.cprb_resid_restrict(C.byref(dl.desc), D.ptr(b), D.ptr(x), D.ptr(rc), st))
+        if cycle == "v" or l + 1 == L - 1:
+            ec = self._cycle_at(l + 1, rc, use_fcg, cycle)
+        else:
+            pre = lambda s: self._cycle_at(l + 1, s, use_fcg, cycle)  # noqa: E731
+            ec = (self._fcg if use_fcg else self._fgmres)(l + 1, rc, pre)
+        N.check(lib.cprb_prolong(C.byref(dl.desc), D.ptr(ec), D.ptr(x), st))
+        for _ in range(p.post_sweeps):
+            N.check(lib.cprb_pgs_scm_pass(C.byref(dl.desc), D.ptr(b), D.ptr(x), 1, 0, st))
+        return x
+
+    def _fcg(self, l, rhs, precond, steps=2):
+        """src/amg.py:177-196 with device vectors."""
+        x = D.zeros(rhs.shape[0])
+        r = rhs.clone()
+        dirs = []
+        for _ in range(steps):
+            if np.sqrt(D.dot(r, r)) == 0.0:
+                break
+            z = precond(r)
+            p = z
+            for pj, apj, pap_j in dirs:
+                coef = D.dot(z, apj) / pap_j
+                q = D.empty(p.shape[0])
+                D.axpy(-coef, pj, p, q)
+                p = q
+            ap = self._spmv_level(l, p)
+            pap = D.dot(p, ap)
+            if pap <= 0.0 or not np.isfinite(pap):
+                break
+            alpha = D.dot(p, r) / pap
+            xn = D.empty(x.shape[0])
+            D.axpy(alpha, p, x, xn)
+            rn = D.empty(r.shape[0])
+            D.axpy(-alpha, ap, r, rn)
+            x, r = xn, rn
+            dirs.append((p, ap, pap))
+        return x
+
+    def _fgmres(self, l, rhs, precond, steps=2):
+        """src/amg.py:199-225 with device vectors (small least squares on host)."""
+        beta = float(np.sqrt(D.dot(rhs, rhs)))
+        if beta == 0.0:
+            return D.zeros(rhs.shape[0])
+        n = rhs.shape[0]
+        v0 = D.empty(n)
+        N.check(N.lib().cprb_div_host(n, D.ptr(rhs), beta, D.ptr(v0), D.stream()))
+        basis, zs = [v0], []
+        H = np.zeros((steps + 1, steps))
+        m_eff = steps
+        for j in range(steps):
+            z = precond(basis[j])
+            zs.append(z)
+            w = self._spmv_level(l, z)
+            for i in range(j + 1):
+                H[i, j] = D.dot(w, basis[i])
+                wn = D.empty(n)
+                D.axpy(-H[i, j], basis[i], w, wn)
+                w = wn
+            H[j + 1, j] = float(np.sqrt(D.dot(w, w)))
+            if H[j + 1, j] == 0.0:
+                m_eff = j + 1
+                break
+            vn = D.empty(n)
+            N.check(N.lib().cprb_div_host(n, D.ptr(w), float(H[j + 1, j]), D.ptr(vn), D.stream()))
+            basis.append(vn)
+        e1 = np.zeros(m_eff + 1)
+        e1[0] = beta
+        y, *_ = np.linalg.lstsq(H[:m_eff + 1, :m_eff], e1, rcond=None)
+        x = D.zeros(n)
+        for i in range(m_eff):
+            xn = D.empty(n)
+            D.axpy(float(y[i]), zs[i], x, xn)
+            x = xn
+        return x
+
+    @property
+    def native_ok(self) -> bool:
+        p = self.h.params
+        return p.pre_sweeps == 1 and p.post_sweeps == 1
+
+    def hostcycle(self, r, z, cycle):
+        """Host-driven cycle (K-cycle, or V with several sweeps) on natural-order
+        device vectors r (stride in_stride) -> z (natural order)."""
+        t = D.torch()
+        if not hasattr(self, "_perm0_t"):
+            self._perm0_t = t.from_numpy(self.perms[0]).to("cuda")
+            self._gidx_t = t.from_numpy(self.perms[0] * self.in_stride).to("cuda")
+        b0 = r.index_select(0, self._gidx_t).contiguous()
+        x = self._cycle_at(0, b0, bool(self.desc.use_fcg), cycle)
+        z[self._perm0_t] = x
+
+    def cycle(self, r, z, cycle):
+        if cycle == "v" and self.native_ok:
+            self.vcycle(r, z)
+        else:
+            self.hostcycle(r, z, cycle)
+
+
+def amg_cycle(h: AmgHierarchy, r, cycle: str | None = None, workers: int = 1):
+    """One multigrid cycle from a zero guess, z ~= A^{-1} r (src/amg.py:228-242)."""
+    if np.shape(r) != (h.fine_size,):
+        raise ValueError(f"dimension mismatch: expected residual of length {h.fine_size}")
+    cycle = cycle or h.params.cycle
+    dev = h.device(1)
+    rd, kind = D.to_device(r)
+    z = D.empty(h.fine_size)
+    dev.cycle(rd, z, cycle)
+    return D.from_device(z, kind)

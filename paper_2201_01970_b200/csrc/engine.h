@@ -1,0 +1,22 @@
+// Internal declarations shared by the .cu translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "../../include/cpr_b200.h"
+
+namespace cprb {
+int set_error(int code, const std::string& msg);
+int check_launch(const char* what);
+
+int bsr_op(int mode, const cprb_sell& A, int b, const double* x, const double* rhs, double* out,
+           int32_t* flag, double* sent, cudaStream_t st);
+int amg_vcycle(const cprb_amg& h, const double* r, double* z, cudaStream_t st);
+int bilu_solve(const cprb_bilu& F, const double* r, double* zl, double* y, const double* zp,
+               double* zout, cudaStream_t st);
+int fill_sentinel(double* p, int64_t n, cudaStream_t st);
+int pgs_pass(const cprb_amg_level& L, const double* b, double* x, int dir, int zero_guess,
+             const double* gather_src, int gather_stride, const int32_t* perm,
+             double* scatter_out, cudaStream_t st);
+}  // namespace cprb

@@ -1,0 +1,493 @@
+// Host-side SETUP of the CPR preconditioner: strong connections, colour
+// grouping, pairwise aggregation, Galerkin products, BILU(0), level
+// schedules, coarsest inverse.  Structural outputs are bit-exact to the
+// reference (cprkit); floating-point sums follow numpy's reduceat order.
+// Compiled with -ffp-contract=off (no FMA contraction).
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <numeric>
+#include <queue>
+#include <string>
+#include <vector>
+
+#include "common.h"
+
+namespace cprb {
+
+// numpy pairwise summation of a contiguous float64 run (the order of
+// np.add.reduce / the reduceat tail).
+double pairwise_sum(const double* a, int64_t n) {
+  if (n < 8) {
+    double s = 0.0;
+    for (int64_t i = 0; i < n; ++i) s += a[i];
+    return s;
+  }
+  if (n <= 128) {
+    double r[8];
+    for (int k = 0; k < 8; ++k) r[k] = a[k];
+    int64_t i = 8;
+    for (; i + 8 <= n; i += 8)
+      for (int k = 0; k < 8; ++k) r[k] += a[i + k];
+    double s = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) s += a[i];
+    return s;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return pairwise_sum(a, n2) + pairwise_sum(a + n2, n - n2);
+}
+
+// one np.add.reduceat segment: a[0] + pairwise(a[1:])
+double segment_sum(const double* a, int64_t n) {
+  if (n <= 0) return 0.0;
+  return a[0] + pairwise_sum(a + 1, n - 1);
+}
+
+}  // namespace cprb
+
+using namespace cprb;
+
+extern "C" {
+
+// src/coloring.py:79-114
+int cprb_strong_connections(int64_t n, const int64_t* ptr, const int64_t* cols,
+                            const double* vals, double theta, int64_t* s_ptr,
+                            int64_t* s_cols) {
+  if (!(theta >= 0.0 && theta <= 1.0))
+    return set_error(CPRB_EINVAL, "theta must lie in [0, 1], got " + std::to_string(theta));
+  std::vector<double> absrow;
+  int64_t k = 0;
+  s_ptr[0] = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t lo = ptr[i], hi = ptr[i + 1];
+    absrow.resize(hi - lo);
+    for (int64_t p = lo; p < hi; ++p) absrow[p - lo] = std::fabs(vals[p]);
+    const double thr = theta * segment_sum(absrow.data(), hi - lo);
+    for (int64_t p = lo; p < hi; ++p)
+      if (cols[p] != i && absrow[p - lo] > thr) s_cols[k++] = cols[p];
+    s_ptr[i + 1] = k;
+  }
+  return CPRB_OK;
+}
+
+// src/coloring.py:238-256, vertices_splitting :171-235.
+int cprb_vertices_grouping(int64_t n, const int64_t* s_ptr, const int64_t* s_cols,
+                           int64_t* perm, int64_t* group_sizes, int64_t* ncolors) {
+  // symmetrised pattern S ∪ S^T (src/coloring.py:58-71), sorted & deduplicated
+  std::vector<int64_t> cnt(n + 1, 0);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t p = s_ptr[i]; p < s_ptr[i + 1]; ++p) {
+      cnt[i + 1]++;
+      cnt[s_cols[p] + 1]++;
+    }
+  for (int64_t i = 0; i < n; ++i) cnt[i + 1] += cnt[i];
+  std::vector<int64_t> adj(cnt[n]);
+  std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t p = s_ptr[i]; p < s_ptr[i + 1]; ++p) {
+      adj[fill[i]++] = s_cols[p];
+      adj[fill[s_cols[p]]++] = i;
+    }
+  std::vector<int64_t> nptr(n + 1, 0);
+  std::vector<int64_t> nadj;
+  nadj.reserve(adj.size());
+  for (int64_t i = 0; i < n; ++i) {
+    auto b = adj.begin() + cnt[i], e = adj.begin() + cnt[i + 1];
+    std::sort(b, e);
+    auto u = std::unique(b, e);
+    nadj.insert(nadj.end(), b, u);
+    nptr[i + 1] = (int64_t)nadj.size();
+  }
+  std::vector<int64_t> infl(n);
+  int64_t maxinfl = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    infl[i] = nptr[i + 1] - nptr[i];
+    maxinfl = std::max(maxinfl, infl[i]);
+  }
+  // priority key: (-influence, index) ascending  <=>  (maxinfl-infl, index)
+  auto key = [&](int64_t v) -> uint64_t {
+    return ((uint64_t)(maxinfl - infl[v]) << 32) | (uint64_t)v;
+  };
+  using MinHeap = std::priority_queue<uint64_t, std::vector<uint64_t>, std::greater<uint64_t>>;
+
+  std::vector<uint8_t> und(n), deferred(n), in_front(n), in_w(n);
+  std::vector<int64_t> vertices(n);
+  std::iota(vertices.begin(), vertices.end(), 0);
+  int64_t out = 0, ng = 0;
+  while (!vertices.empty()) {
+    std::fill(und.begin(), und.end(), 0);
+    std::fill(deferred.begin(), deferred.end(), 0);
+    std::fill(in_front.begin(), in_front.end(), 0);
+    std::fill(in_w.begin(), in_w.end(), 0);
+    std::vector<uint64_t> vk;
+    vk.reserve(vertices.size());
+    for (int64_t v : vertices) {
+      und[v] = 1;
+      vk.push_back(key(v));
+    }
+    MinHeap vheap(std::greater<uint64_t>(), std::move(vk));
+    MinHeap fheap;
+    std::vector<int64_t> w;
+    int64_t remaining = (int64_t)vertices.size();
+    while (remaining > 0) {
+      int64_t v = -1;
+      while (!fheap.empty()) {
+        int64_t c = (int64_t)(fheap.top() & 0xffffffffu);
+        fheap.pop();
+        if (in_front[c] && und[c]) {
+          in_front[c] = 0;
+          v = c;
+          break;
+        }
+        in_front[c] = 0;
+      }
+      if (v < 0) {
+        while (!vheap.empty()) {
+          int64_t c = (int64_t)(vheap.top() & 0xffffffffu);
+          vheap.pop();
+          if (und[c]) {
+            v = c;
+            break;
+          }
+        }
+        if (v < 0) break;
+      }
+      bool touches = false;
+      for (int64_t p = nptr[v]; p < nptr[v + 1]; ++p)
+        if (in_w[nadj[p]]) { touches = true; break; }
+      if (touches) {
+        deferred[v] = 1;
+        und[v] = 0;
+        --remaining;
+        continue;
+      }
+      in_w[v] = 1;
+      w.push_back(v);
+      und[v] = 0;
+      --remaining;
+      for (int64_t p = nptr[v]; p < nptr[v + 1]; ++p) {
+        int64_t k = nadj[p];
+        if (und[k]) {
+          deferred[k] = 1;
+          und[k] = 0;
+          --remaining;
+        }
+      }
+      for (int64_t p = nptr[v]; p < nptr[v + 1]; ++p) {
+        int64_t k = nadj[p];
+        for (int64_t q = nptr[k]; q < nptr[k + 1]; ++q) {
+          int64_t j = nadj[q];
+          if (und[j] && !in_front[j] && j != v) {
+            in_front[j] = 1;
+            fheap.push(key(j));
+          }
+        }
+      }
+    }
+    if (w.empty()) return set_error(CPRB_ERUNTIME, "vertices_splitting returned an empty group");
+    std::sort(w.begin(), w.end());
+    for (int64_t v : w) perm[out++] = v;
+    group_sizes[ng++] = (int64_t)w.size();
+    std::vector<int64_t> wbar;
+    for (int64_t v = 0; v < n; ++v)
+      if (deferred[v]) wbar.push_back(v);
+    vertices.swap(wbar);
+  }
+  *ncolors = ng;
+  return CPRB_OK;
+}
+
+// src/amg.py:89-119
+int cprb_pairwise_aggregate(int64_t n, const int64_t* ptr, const int64_t* cols,
+                            const double* vals, double theta_amg, int64_t* agg,
+                            int64_t* n_agg) {
+  std::vector<int64_t> sptr(n + 1), scols(ptr[n] > 0 ? ptr[n] : 1);
+  int rc = cprb_strong_connections(n, ptr, cols, vals, theta_amg, sptr.data(), scols.data());
+  if (rc) return rc;
+  auto find = [&](int64_t row, int64_t col) -> int64_t {
+    const int64_t* b = cols + ptr[row];
+    const int64_t* e = cols + ptr[row + 1];
+    const int64_t* it = std::lower_bound(b, e, col);
+    return (it != e && *it == col) ? (int64_t)(it - cols) : -1;
+  };
+  for (int64_t i = 0; i < n; ++i) agg[i] = -1;
+  int64_t na = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (agg[i] >= 0) continue;
+    int64_t best = -1;
+    double bw = 0.0;
+    for (int64_t p = sptr[i]; p < sptr[i + 1]; ++p) {
+      int64_t j = scols[p];
+      if (agg[j] >= 0) continue;
+      // W = |A| + |A|^T via duplicate-summing COO: |a_ij| first, then |a_ji|
+      int64_t pij = find(i, j), pji = find(j, i);
+      double wgt = std::fabs(vals[pij]);
+      if (pji >= 0) wgt = wgt + (0.0 + std::fabs(vals[pji]));
+      if (best < 0 || wgt > bw) {
+        best = j;
+        bw = wgt;
+      }
+    }
+    if (best >= 0) agg[best] = na;
+    agg[i] = na;
+    ++na;
+  }
+  *n_agg = na;
+  return CPRB_OK;
+}
+
+// src/amg.py:127-132 via CsrMatrix.from_coo(sum_duplicates=True)
+// (src/sparse.py:88-110): stable order = fine row-major inside each (I, J).
+int cprb_galerkin(int64_t n, const int64_t* ptr, const int64_t* cols, const double* vals,
+                  const int64_t* agg, int64_t n_agg, int64_t* c_ptr, int64_t* c_cols,
+                  double* c_vals, int64_t* c_nnz) {
+  const int64_t nnz = ptr[n];
+  // stable counting sort of entries by coarse row I
+  std::vector<int64_t> rcnt(n_agg + 1, 0);
+  for (int64_t i = 0; i < n; ++i) rcnt[agg[i] + 1] += ptr[i + 1] - ptr[i];
+  for (int64_t I = 0; I < n_agg; ++I) rcnt[I + 1] += rcnt[I];
+  std::vector<int64_t> order(nnz);
+  {
+    std::vector<int64_t> fill(rcnt.begin(), rcnt.end() - 1);
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t p = ptr[i]; p < ptr[i + 1]; ++p) order[fill[agg[i]]++] = p;
+  }
+  std::vector<double> run;
+  int64_t k = 0;
+  c_ptr[0] = 0;
+  for (int64_t I = 0; I < n_agg; ++I) {
+    auto b = order.begin() + rcnt[I], e = order.begin() + rcnt[I + 1];
+    std::stable_sort(b, e, [&](int64_t x, int64_t y) { return agg[cols[x]] < agg[cols[y]]; });
+    for (auto it = b; it != e;) {
+      const int64_t J = agg[cols[*it]];
+      run.clear();
+      auto jt = it;
+      while (jt != e && agg[cols[*jt]] == J) run.push_back(vals[*jt++]);
+      c_cols[k] = J;
+      c_vals[k] = segment_sum(run.data(), (int64_t)run.size());
+      ++k;
+      it = jt;
+    }
+    c_ptr[I + 1] = k;
+  }
+  *c_nnz = k;
+  return CPRB_OK;
+}
+
+// src/amg.py:135-140
+int cprb_is_symmetric(int64_t n, const int64_t* ptr, const int64_t* cols, const double* vals,
+                      double tol, int32_t* out) {
+  double scale = 0.0, diff = 0.0;
+  bool nan = false;
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t p = ptr[i]; p < ptr[i + 1]; ++p) {
+      const int64_t j = cols[p];
+      const int64_t* b = cols + ptr[j];
+      const int64_t* e = cols + ptr[j + 1];
+      const int64_t* it = std::lower_bound(b, e, i);
+      if (it == e || *it != i) {
+        *out = 0;
+        return CPRB_OK;
+      }
+      const double a = vals[p], t = vals[it - cols];
+      if (std::isnan(a) || std::isnan(t)) nan = true;
+      scale = std::max(scale, std::fabs(a));
+      diff = std::max(diff, std::fabs(a - t));
+    }
+  *out = (!nan && diff <= tol * std::max(scale, 1.0)) ? 1 : 0;
+  return CPRB_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// src/sparse.py:372-396 (Gauss-Jordan with partial pivoting; same elementwise
+// operation sequence, so bitwise equal).  Returns false on an exact zero pivot.
+bool gj_invert(int b, const double* blk, double* inv) {
+  double a[64], v[64];
+  for (int i = 0; i < b * b; ++i) a[i] = blk[i];
+  for (int r = 0; r < b; ++r)
+    for (int c = 0; c < b; ++c) v[r * b + c] = (r == c) ? 1.0 : 0.0;
+  for (int col = 0; col < b; ++col) {
+    int p = col;
+    double best = std::fabs(a[col * b + col]);
+    for (int r = col + 1; r < b; ++r)
+      if (std::fabs(a[r * b + col]) > best) {
+        best = std::fabs(a[r * b + col]);
+        p = r;
+      }
+    if (a[p * b + col] == 0.0) return false;
+    if (p != col)
+      for (int c = 0; c < b; ++c) {
+        std::swap(a[col * b + c], a[p * b + c]);
+        std::swap(v[col * b + c], v[p * b + c]);
+      }
+    const double piv = a[col * b + col];
+    for (int c = 0; c < b; ++c) {
+      a[col * b + c] /= piv;
+      v[col * b + c] /= piv;
+    }
+    for (int r = 0; r < b; ++r) {
+      if (r == col) continue;
+      const double f = a[r * b + col];
+      if (f != 0.0)
+        for (int c = 0; c < b; ++c) {
+          a[r * b + c] = a[r * b + c] - f * a[col * b + c];
+          v[r * b + c] = v[r * b + c] - f * v[col * b + c];
+        }
+    }
+  }
+  for (int i = 0; i < b * b; ++i) inv[i] = v[i];
+  return true;
+}
+
+inline void matmul(int b, const double* x, const double* y, double* out) {
+  for (int i = 0; i < b; ++i)
+    for (int l = 0; l < b; ++l) {
+      double s = 0.0;
+      for (int j = 0; j < b; ++j) s = s + x[i * b + j] * y[j * b + l];
+      out[i * b + l] = s;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int cprb_invert_small_blocks(int64_t m, int32_t b, const double* blocks, double* out) {
+  if (b < 1 || b > 8) return set_error(CPRB_EINVAL, "block size must be 1..8");
+  for (int64_t k = 0; k < m; ++k)
+    if (!gj_invert(b, blocks + k * b * b, out + k * b * b))
+      return set_error(CPRB_ESINGULAR, "singular diagonal block at row " + std::to_string(k));
+  return CPRB_OK;
+}
+
+// src/ilu.py:150-193 (+ _invert_pivot :134-147)
+int cprb_bilu0_factorize(int64_t n, int32_t b, const int64_t* ptr, const int64_t* cols,
+                         double* vals, double* uinv, int64_t* perturbed,
+                         int64_t* n_perturbed) {
+  if (b < 1 || b > 8) return set_error(CPRB_EINVAL, "block size must be 1..8");
+  const int bb = b * b;
+  int64_t npert = 0;
+  double tmp[64];
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t lo = ptr[i], hi = ptr[i + 1];
+    const int64_t* rb = cols + lo;
+    const int64_t dk = std::lower_bound(rb, cols + hi, i) - rb;
+    if (lo + dk >= hi || cols[lo + dk] != i)
+      return set_error(CPRB_EINVAL, "diagonal block missing in row " + std::to_string(i));
+    for (int64_t p = lo; p < lo + dk; ++p) {
+      const int64_t k = cols[p];
+      matmul(b, vals + p * bb, uinv + k * bb, tmp);
+      std::memcpy(vals + p * bb, tmp, sizeof(double) * bb);
+      const int64_t klo = ptr[k], khi = ptr[k + 1];
+      int64_t pos = klo;
+      for (int64_t q = p + 1; q < hi; ++q) {
+        const int64_t j = cols[q];
+        while (pos < khi && cols[pos] < j) ++pos;
+        if (pos < khi && cols[pos] == j) {
+          matmul(b, vals + p * bb, vals + pos * bb, tmp);
+          for (int e = 0; e < bb; ++e) vals[q * bb + e] = vals[q * bb + e] - tmp[e];
+        }
+      }
+    }
+    const double* piv = vals + (lo + dk) * bb;
+    if (!gj_invert(b, piv, uinv + i * bb)) {
+      double sq[64];
+      for (int e = 0; e < bb; ++e) sq[e] = piv[e] * piv[e];
+      const double fro = std::sqrt(pairwise_sum(sq, bb));
+      if (fro == 0.0)
+        return set_error(CPRB_ESINGULAR, "singular pivot block at row " + std::to_string(i));
+      const double t = 1e-8 * fro;
+      double bumped[64];
+      for (int r = 0; r < b; ++r)
+        for (int c = 0; c < b; ++c)
+          bumped[r * b + c] = piv[r * b + c] + (r == c ? t * 1.0 : t * 0.0);
+      if (!gj_invert(b, bumped, uinv + i * bb))
+        return set_error(CPRB_ESINGULAR, "singular pivot block at row " + std::to_string(i));
+      perturbed[npert++] = i;
+    }
+  }
+  *n_perturbed = npert;
+  return CPRB_OK;
+}
+
+// src/ilu.py:38-59
+int cprb_level_schedule(int64_t n, const int64_t* ptr, const int64_t* cols, int64_t* level,
+                        int64_t* nlevels) {
+  bool any_below = false, any_above = false;
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t p = ptr[i]; p < ptr[i + 1]; ++p) {
+      if (cols[p] < i) any_below = true;
+      if (cols[p] > i) any_above = true;
+    }
+  if (any_below && any_above)
+    return set_error(CPRB_EINVAL, "pattern is neither lower nor upper triangular");
+  const bool lower = !any_above;
+  int64_t maxl = 0;
+  for (int64_t t = 0; t < n; ++t) {
+    const int64_t i = lower ? t : n - 1 - t;
+    int64_t m = 0;
+    for (int64_t p = ptr[i]; p < ptr[i + 1]; ++p)
+      if (cols[p] != i) m = std::max(m, level[cols[p]]);
+    level[i] = 1 + m;
+    maxl = std::max(maxl, level[i]);
+  }
+  *nlevels = n > 0 ? maxl : 1;
+  return CPRB_OK;
+}
+
+// Coarsest solve operator: inverse of a dense n x n matrix via LU with
+// partial pivoting (first max |pivot|, the LAPACK getrf rule), then
+// forward/back substitution of the identity columns.
+int cprb_dense_inverse(int64_t n, const double* a_in, double* inv) {
+  std::vector<double> a(a_in, a_in + n * n);
+  std::vector<int64_t> piv(n);
+  for (int64_t k = 0; k < n; ++k) {
+    int64_t p = k;
+    double best = std::fabs(a[k * n + k]);
+    for (int64_t r = k + 1; r < n; ++r)
+      if (std::fabs(a[r * n + k]) > best) {
+        best = std::fabs(a[r * n + k]);
+        p = r;
+      }
+    if (!std::isfinite(best))
+      return set_error(CPRB_ERUNTIME, "coarsest-level dense factorization failed: non-finite entries");
+    if (best == 0.0)
+      return set_error(CPRB_ERUNTIME, "coarsest-level dense factorization failed: singular matrix");
+    piv[k] = p;
+    if (p != k)
+      for (int64_t c = 0; c < n; ++c) std::swap(a[k * n + c], a[p * n + c]);
+    const double d = a[k * n + k];
+    for (int64_t r = k + 1; r < n; ++r) {
+      const double l = a[r * n + k] / d;
+      a[r * n + k] = l;
+      if (l != 0.0)
+        for (int64_t c = k + 1; c < n; ++c) a[r * n + c] -= l * a[k * n + c];
+    }
+  }
+  std::vector<double> col(n);
+  for (int64_t e = 0; e < n; ++e) {
+    std::fill(col.begin(), col.end(), 0.0);
+    col[e] = 1.0;
+    for (int64_t k = 0; k < n; ++k)
+      if (piv[k] != k) std::swap(col[k], col[piv[k]]);
+    for (int64_t r = 0; r < n; ++r) {
+      double s = col[r];
+      for (int64_t c = 0; c < r; ++c) s -= a[r * n + c] * col[c];
+      col[r] = s;
+    }
+    for (int64_t r = n - 1; r >= 0; --r) {
+      double s = col[r];
+      for (int64_t c = r + 1; c < n; ++c) s -= a[r * n + c] * col[c];
+      col[r] = s / a[r * n + r];
+    }
+    for (int64_t r = 0; r < n; ++r) inv[r * n + e] = col[r];
+  }
+  return CPRB_OK;
+}
+
+}  // extern "C"

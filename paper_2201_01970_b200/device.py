@@ -1,0 +1,244 @@
+"""Device plumbing: vectors, SELL-32 layouts and the device plans the C ABI
+consumes.
+
+PyTorch owns device memory and the stream; the sm_100a library does all the
+arithmetic.  Layout builders here are host-side numpy (setup time only): they
+rearrange stored values without changing any of them, and keep each row's
+entries in the order the reference sums them.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+
+_torch = None
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as t
+        _torch = t
+    return _torch
+
+
+def require_cuda():
+    t = torch()
+    if not t.cuda.is_available():
+        raise RuntimeError("the CPR-GMRES solve path needs a CUDA device (B200); there is no "
+                           "CPU fallback")
+    N.lib()
+
+
+def stream() -> int:
+    return torch().cuda.current_stream().cuda_stream
+
+
+def ptr(t) -> int:
+    return 0 if t is None else int(t.data_ptr())
+
+
+def empty(n: int, dtype=None):
+    t = torch()
+    return t.empty(int(n), dtype=dtype or t.float64, device="cuda")
+
+
+def zeros(n: int, dtype=None):
+    t = torch()
+    return t.zeros(int(n), dtype=dtype or t.float64, device="cuda")
+
+
+def to_device(x):
+    """(CUDA float64 tensor, kind) for a numpy array / host tensor / CUDA tensor.
+    kind tells from_device how to hand results back."""
+    require_cuda()
+    t = torch()
+    if isinstance(x, t.Tensor):
+        if x.is_cuda:
+            if x.dtype != t.float64 or not x.is_contiguous():
+                x = x.to(t.float64).contiguous()
+            return x, "cuda"
+        return x.to(device="cuda", dtype=t.float64, non_blocking=x.is_pinned()), "host_tensor"
+    a = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+    return t.from_numpy(a).to("cuda"), "numpy"
+
+
+def from_device(y, kind):
+    if kind == "cuda":
+        return y
+    if kind == "host_tensor":
+        return y.cpu()
+    return y.cpu().numpy()
+
+
+def upload(a: np.ndarray, dtype=None):
+    t = torch()
+    a = np.ascontiguousarray(a)
+    return t.from_numpy(a).to("cuda")
+
+
+# -- reductions / vector ops -------------------------------------------------
+
+
+class _Scratch:
+    def __init__(self):
+        t = torch()
+        self.partials = t.zeros(N_RED, dtype=t.float64, device="cuda")
+        self.ticket = t.zeros(4, dtype=t.int32, device="cuda")
+        self.out = t.zeros(64, dtype=t.float64, device="cuda")
+
+
+N_RED = 1184
+_scratch = {}
+
+
+def scratch() -> _Scratch:
+    dev = torch().cuda.current_device()
+    if dev not in _scratch:
+        _scratch[dev] = _Scratch()
+    return _scratch[dev]
+
+
+def dot(x, y) -> float:
+    s = scratch()
+    N.check(N.lib().cprb_dot(x.shape[0], ptr(x), ptr(y), ptr(s.out), ptr(s.partials),
+                             ptr(s.ticket), stream()))
+    return float(s.out[0].item())
+
+
+def dot_dev(x, y, out, s=None):
+    """(x, y) into the device scalar `out` (no host sync)."""
+    s = s or scratch()
+    N.check(N.lib().cprb_dot(x.shape[0], ptr(x), ptr(y), ptr(out), ptr(s.partials),
+                             ptr(s.ticket), stream()))
+
+
+def axpy(alpha: float, x, y, out):
+    N.check(N.lib().cprb_axpy(x.shape[0], float(alpha), ptr(x), ptr(y), ptr(out), stream()))
+
+
+# -- SELL-32 packing -----------------------------------------------------------
+
+
+def pad_lanes(rows: np.ndarray) -> np.ndarray:
+    """Pad a lane->row list with -1 to a multiple of 32."""
+    L = rows.shape[0]
+    P = (-L) % 32
+    if P:
+        rows = np.concatenate([rows, np.full(P, -1, dtype=rows.dtype)])
+    return rows
+
+
+@dataclass
+class SellHost:
+    nslices: int
+    nrows: int
+    slice_ptr: np.ndarray
+    lane_row: np.ndarray
+    lane_len: np.ndarray
+    cols: np.ndarray
+    vals: np.ndarray
+    lane_len_lo: np.ndarray | None = None
+    agg_out: np.ndarray | None = None
+
+
+def pack_sell(lane_row, lane_ptr, ent_cols, ent_vals, bs, nrows, lane_len_lo=None,
+              agg_out=None) -> SellHost:
+    """Pack per-lane entry lists into SELL-32.
+
+    lane_row: (L,) rows (L % 32 == 0, -1 = padding); lane_ptr: (L+1,) entry
+    offsets of each lane's list in ent_cols/ent_vals; ent_vals (nnz,) scalars or
+    (nnz, bs, bs) blocks.  Entry m of lane l lands at slice_ptr[s] + 32m + l;
+    block value (r, c) at (slice_ptr[s] + 32m)*bs*bs + (r*bs + c)*32 + l.
+    """
+    lane_row = np.asarray(lane_row, dtype=np.int32)
+    L = lane_row.shape[0]
+    assert L % 32 == 0
+    ns = L // 32
+    lens = np.diff(np.asarray(lane_ptr, dtype=np.int64)).astype(np.int64)
+    width = lens.reshape(ns, 32).max(axis=1) if ns else np.zeros(0, dtype=np.int64)
+    slice_ptr = np.zeros(ns + 1, dtype=np.int64)
+    np.cumsum(width * 32, out=slice_ptr[1:])
+    total = int(slice_ptr[-1])
+    nnz = int(lens.sum())
+    lane_of = np.repeat(np.arange(L, dtype=np.int64), lens)
+    m = np.arange(nnz, dtype=np.int64) - np.asarray(lane_ptr, dtype=np.int64)[lane_of]
+    s = lane_of // 32
+    lane = lane_of % 32
+    d = slice_ptr[s] + m * 32 + lane
+    cols = np.zeros(max(total, 1), dtype=np.int32)
+    cols[d] = ent_cols
+    bb = bs * bs
+    vals = np.zeros(max(total * bb, 1))
+    if bb == 1:
+        vals[d] = np.asarray(ent_vals, dtype=np.float64).reshape(-1)
+    else:
+        e = np.arange(bb, dtype=np.int64)
+        idx = ((d - lane) * bb)[:, None] + e[None, :] * 32 + lane[:, None]
+        vals[idx.reshape(-1)] = np.asarray(ent_vals, dtype=np.float64).reshape(-1)
+    return SellHost(ns, int(nrows), slice_ptr, lane_row, lens.astype(np.int32), cols, vals,
+                    None if lane_len_lo is None else np.asarray(lane_len_lo, dtype=np.int32),
+                    None if agg_out is None else np.asarray(agg_out, dtype=np.int32))
+
+
+class SellDev:
+    """Device copy of a SellHost plus its C descriptor."""
+
+    def __init__(self, h: SellHost):
+        self.host = h
+        self.t = {k: upload(getattr(h, k)) for k in
+                  ("slice_ptr", "lane_row", "lane_len", "cols", "vals")}
+        for k in ("lane_len_lo", "agg_out"):
+            v = getattr(h, k)
+            self.t[k] = upload(v) if v is not None else None
+        self.desc = N.Sell(h.nslices, h.nrows, ptr(self.t["slice_ptr"]), ptr(self.t["lane_row"]),
+                           ptr(self.t["lane_len"]), ptr(self.t["lane_len_lo"]),
+                           ptr(self.t["cols"]), ptr(self.t["vals"]), ptr(self.t["agg_out"]))
+
+    def nbytes(self) -> int:
+        return sum(int(v.numel() * v.element_size()) for v in self.t.values() if v is not None)
+
+
+def sell_rows(ptr_, cols, vals, bs, nrows) -> SellHost:
+    """SELL-32 of a (block) CSR in natural row order."""
+    lane_row = pad_lanes(np.arange(nrows, dtype=np.int32))
+    lp = np.zeros(lane_row.shape[0] + 1, dtype=np.int64)
+    lp[1:nrows + 1] = ptr_[1:]
+    lp[nrows + 1:] = ptr_[-1]
+    return pack_sell(lane_row, lp, cols, vals, bs, nrows)
+
+
+class DeviceMatrix:
+    """A CsrMatrix / BlockCsrMatrix resident on the device (SELL-32)."""
+
+    def __init__(self, A):
+        require_cuda()
+        bs = int(getattr(A, "block_size", 1))
+        self.b = bs
+        self.nrows = int(A.nrows)
+        vals = np.asarray(A.values, dtype=np.float64)
+        if bs == 1:
+            vals = vals.reshape(-1)
+        self.sell = SellDev(sell_rows(np.asarray(A.row_ptr, dtype=np.int64),
+                                      np.asarray(A.col_idx), vals, bs, A.nrows))
+
+    def desc_ref(self):
+        return C.byref(self.sell.desc)
+
+
+def device_matrix(A) -> DeviceMatrix:
+    """Device copy cached on the matrix object (matrices are immutable after
+    construction in the reference's contract, src/sparse.py:217-218)."""
+    M = getattr(A, "_cprb_dev", None)
+    if M is None:
+        M = DeviceMatrix(A)
+        try:
+            object.__setattr__(A, "_cprb_dev", M)
+        except (AttributeError, TypeError):
+            pass
+    return M

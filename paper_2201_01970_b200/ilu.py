@@ -1,0 +1,189 @@
+"""Block ILU(0) (drop-in for cprkit.ilu).
+
+SETUP (host C++): the IKJ factorization restricted to the pattern, pivot
+inversion with the reference's perturbation fallback, level schedules
+(src/ilu.py:38-193).  SOLVE (device): sync-free level-ordered L and U
+substitutions (csrc/bilu.cu), bitwise equal to the reference's
+level-scheduled solve for the same factors.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from . import device as D
+from .sparse import BlockCsrMatrix, CsrMatrix, to_block
+
+__all__ = ["BiluFactors", "LevelSchedule", "bilu0_factorize", "level_schedule", "bilu_apply"]
+
+
+@dataclass
+class LevelSchedule:
+    levels: list
+
+    @property
+    def n_levels(self) -> int:
+        return len(self.levels)
+
+
+def _levels_from(level: np.ndarray, nlev: int) -> list:
+    order = np.argsort(level, kind="stable")
+    counts = np.bincount(level, minlength=nlev + 1)[1:]
+    bounds = np.concatenate([[0], np.cumsum(counts)])
+    return [order[bounds[i]:bounds[i + 1]].astype(np.int64) for i in range(nlev)]
+
+
+def level_schedule(T) -> LevelSchedule:
+    """level(i) = 1 + max level of the in-pattern predecessors (src/ilu.py:38-59)."""
+    n = T.nrows
+    ptr = np.ascontiguousarray(T.row_ptr, dtype=np.int64)
+    cols = np.ascontiguousarray(T.col_idx, dtype=np.int64)
+    level = np.zeros(max(n, 1), dtype=np.int64)
+    nl = np.zeros(1, dtype=np.int64)
+    N.check(N.lib().cprb_level_schedule(n, N.p64(ptr), N.p64(cols if cols.size else np.zeros(1, np.int64)),
+                                        N.p64(level), N.p64(nl)))
+    return LevelSchedule(_levels_from(level[:n], int(nl[0])) if n else [np.zeros(0, np.int64)])
+
+
+@dataclass
+class BiluFactors:
+    """L (unit lower) and U (upper) on A's pattern, inverted U diagonal
+    (src/ilu.py:110-131)."""
+
+    L: BlockCsrMatrix
+    U: BlockCsrMatrix
+    block_size: int
+    u_diag_inv: np.ndarray
+    l_schedule: LevelSchedule
+    u_schedule: LevelSchedule
+    _dev: object = field(default=None, repr=False)
+
+    @property
+    def n(self) -> int:
+        return self.L.nrows
+
+    def device(self) -> "DeviceBilu":
+        if self._dev is None:
+            self._dev = DeviceBilu(self)
+        return self._dev
+
+
+def bilu0_factorize(A) -> BiluFactors:
+    """ILU(0) with no fill (src/ilu.py:150-193); a singular pivot with a nonzero
+    Frobenius norm is perturbed by 1e-8*||B||_F*I with a RuntimeWarning."""
+    if isinstance(A, CsrMatrix) or np.ndim(getattr(A, "values", None)) == 1:
+        A = to_block(A if isinstance(A, CsrMatrix) else CsrMatrix(A.nrows, A.ncols, A.row_ptr,
+                                                                     A.col_idx, A.values))
+    n, b = A.nrows, A.block_size
+    if A.nrows != A.ncols:
+        raise ValueError("factorization needs a square matrix")
+    ptr = np.ascontiguousarray(A.row_ptr, dtype=np.int64)
+    cols = np.ascontiguousarray(A.col_idx, dtype=np.int64)
+    vals = np.ascontiguousarray(A.values, dtype=np.float64).copy()
+    uinv = np.zeros((n, b, b))
+    pert = np.zeros(max(n, 1), dtype=np.int64)
+    npert = np.zeros(1, dtype=np.int64)
+    N.check(N.lib().cprb_bilu0_factorize(n, b, N.p64(ptr), N.p64(cols if cols.size else np.zeros(1, np.int64)),
+                                         N.pf64(vals.reshape(-1) if vals.size else np.zeros(1)),
+                                         N.pf64(uinv.reshape(-1) if uinv.size else np.zeros(1)),
+                                         N.p64(pert), N.p64(npert)))
+    for row in pert[:int(npert[0])]:
+        N.warn(f"bilu0: perturbing singular pivot block at row {int(row)}", RuntimeWarning, 2)
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(ptr))
+    lower = cols < rows
+    # L: strict lower then the identity diagonal (already column-sorted per row)
+    nlow = np.bincount(rows[lower], minlength=n)
+    lptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(nlow + 1, out=lptr[1:])
+    lcols = np.empty(lptr[-1], dtype=np.int64)
+    lvals = np.empty((lptr[-1], b, b))
+    diag_pos = lptr[1:] - 1
+    is_diag = np.zeros(lptr[-1], dtype=bool)
+    is_diag[diag_pos] = True
+    lcols[~is_diag] = cols[lower]
+    lvals[~is_diag] = vals[lower]
+    lcols[diag_pos] = np.arange(n)
+    lvals[diag_pos] = np.eye(b)
+    L = BlockCsrMatrix(b, n, n, lptr, lcols, lvals)
+    uptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows[~lower], minlength=n), out=uptr[1:])
+    U = BlockCsrMatrix(b, n, n, uptr, cols[~lower].copy(), vals[~lower].copy())
+    return BiluFactors(L, U, b, uinv, level_schedule(L), level_schedule(U))
+
+
+def _strict(T: BlockCsrMatrix):
+    rows = np.repeat(np.arange(T.nrows, dtype=np.int64), np.diff(T.row_ptr))
+    off = rows != T.col_idx
+    ptr = np.zeros(T.nrows + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows[off], minlength=T.nrows), out=ptr[1:])
+    return ptr, T.col_idx[off], T.values[off]
+
+
+def _level_sell(T: BlockCsrMatrix, sched: LevelSchedule, b: int, uinv=None):
+    ptr, cols, vals = _strict(T)
+    lanes = [D.pad_lanes(lv.astype(np.int32)) for lv in sched.levels if lv.shape[0]]
+    lane_row = np.concatenate(lanes) if lanes else np.zeros(0, dtype=np.int32)
+    L = lane_row.shape[0]
+    real = lane_row >= 0
+    lr = lane_row.astype(np.int64)
+    lens = np.zeros(L, dtype=np.int64)
+    lens[real] = np.diff(ptr)[lr[real]]
+    lane_ptr = np.zeros(L + 1, dtype=np.int64)
+    np.cumsum(lens, out=lane_ptr[1:])
+    nnz = int(lane_ptr[-1])
+    lane_of = np.repeat(np.arange(L, dtype=np.int64), lens)
+    src = ptr[lr[lane_of]] + (np.arange(nnz, dtype=np.int64) - lane_ptr[lane_of])
+    h = D.pack_sell(lane_row, lane_ptr, cols[src], vals[src] if b > 1 else vals[src].reshape(-1),
+                    b, T.nrows)
+    ui = None
+    if uinv is not None:
+        bb = b * b
+        ui = np.zeros(max(L * bb, 1))
+        l_idx = np.flatnonzero(real)
+        s, ln = l_idx // 32, l_idx % 32
+        e = np.arange(bb)
+        idx = (s[:, None] * bb + e[None, :]) * 32 + ln[:, None]
+        ui[idx.reshape(-1)] = uinv.reshape(-1, bb)[lr[real]].reshape(-1)
+    return h, ui
+
+
+class DeviceBilu:
+    """Level-ordered SELL-32 copies of the strict L and U factors."""
+
+    def __init__(self, F: BiluFactors):
+        D.require_cuda()
+        b = F.block_size
+        if b not in (1, 3):
+            raise NotImplementedError(f"device BILU supports block sizes 1 and 3, got {b}")
+        hl, _ = _level_sell(F.L, F.l_schedule, b)
+        hu, ui = _level_sell(F.U, F.u_schedule, b, F.u_diag_inv)
+        self.L = D.SellDev(hl)
+        self.U = D.SellDev(hu)
+        self.uinv = D.upload(ui)
+        t = D.torch()
+        self.tickets = t.zeros(4, dtype=t.int32, device="cuda")
+        self.work = D.empty(max(F.n * b, 1))
+        self.desc = N.Bilu(F.n, b, self.L.desc, self.U.desc, D.ptr(self.uinv), D.ptr(self.tickets))
+        self.n, self.b = F.n, b
+
+    def apply(self, r, z):
+        N.check(N.lib().cprb_bilu_apply(C.byref(self.desc), D.ptr(r), D.ptr(z), D.ptr(self.work),
+                                        D.stream()))
+
+
+def bilu_apply(F: BiluFactors, r, workers: int = 1, sequential: bool = False):
+    """z = U^{-1} L^{-1} r (src/ilu.py:196-223).  The device solve is bitwise
+    equal to both of the reference's paths, so `sequential` only selects the
+    same result."""
+    n, b = F.n, F.block_size
+    if np.shape(r) != (n * b,):
+        raise ValueError(f"dimension mismatch: expected vector of length {n * b}")
+    dev = F.device()
+    rd, kind = D.to_device(r)
+    z = D.empty(n * b)
+    dev.apply(rd, z)
+    return D.from_device(z, kind)

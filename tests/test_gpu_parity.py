@@ -1,0 +1,343 @@
+"""Device (sm_100a) parity against the oracle and the reference's fixtures.
+
+Bit-exact where the reference is deterministic (SpMV, smoother sweeps, BILU
+solves for identical factors, residual/restriction); solve-level parity per
+BASELINE.json north_star: same iteration counts, Givens residual history
+within 1e-8 relative, solutions within 1e-6 relative (tighter where the
+fixtures allow)."""
+
+import json
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, load_golden, orc, poisson_2d, random_block, random_sparse, tridiag
+
+import paper_2201_01970_b200 as P
+from paper_2201_01970_b200.ilu import _strict
+
+pytestmark = pytest.mark.gpu
+SUMMARY = json.loads((GOLDEN / "summary.json").read_text())
+
+
+def _csr(o):
+    return P.CsrMatrix(o.nrows, o.ncols, o.ptr, o.cols, o.vals)
+
+
+def _bsr(o):
+    return P.BlockCsrMatrix(o.b, o.nrows, o.ncols, o.ptr, o.cols, o.vals)
+
+
+def _c1():
+    g = load_golden("gen_c1.npz")
+    return P.BlockCsrMatrix(3, 1000, 1000, g["ptr"], g["cols"], g["vals"]), g["b"]
+
+
+def _oracle_bilu(F):
+    lp, lc, lv = _strict(F.L)
+    up, uc, uv = _strict(F.U)
+    return orc.Bilu(F.n, F.block_size, lp, lc, lv, up, uc, uv, F.u_diag_inv,
+                    F.l_schedule.levels, F.u_schedule.levels)
+
+
+# -- K1: SpMV ----------------------------------------------------------------
+
+
+def test_spmv_block_bitwise(gpu):
+    g = load_golden("random_block.npz")
+    for ci in range(int(g["ncases"])):
+        p = f"c{ci}_"
+        n = g[p + "ptr"].shape[0] - 1
+        A = P.BlockCsrMatrix(3, n, n, g[p + "ptr"], g[p + "cols"], g[p + "vals"])
+        assert np.array_equal(P.spmv(A, g[p + "x"]), g[p + "spmv"]), ci
+
+
+def test_spmv_scalar_bitwise(gpu):
+    g = load_golden("random_scalar.npz")
+    for ci in range(int(g["ncases"])):
+        p = f"c{ci}_"
+        n = g[p + "ptr"].shape[0] - 1
+        A = P.CsrMatrix(n, n, g[p + "ptr"], g[p + "cols"], g[p + "vals"])
+        assert np.array_equal(P.spmv(A, g[p + "x0"]), g[p + "spmv"]), ci
+
+
+def test_spmv_c1_rhs_and_long_rows(gpu):
+    A, b = _c1()
+    gen = P.generate_blackoil_like_sequence(10, 10, 10, 1, 0.01, 0)
+    assert np.array_equal(P.spmv(A, P.problems.manufactured_solution(1000)), b)
+    rng = np.random.default_rng(9)
+    for n, avg in ((1, 1), (40, 30), (300, 60), (200, 150)):       # rows beyond 8 blocks / 129 entries
+        M = random_sparse(rng, n, avg_nnz=avg, dominant=False)
+        x = rng.standard_normal(n)
+        assert np.array_equal(P.spmv(_csr(M), x), orc.spmv(M, x)), n
+        B = random_block(rng, max(n // 3, 1), b=3, avg_nnz=min(avg, 40))
+        xb = rng.standard_normal(B.nrows * 3)
+        assert np.array_equal(P.spmv(_bsr(B), xb), orc.spmv(B, xb)), n
+    del gen
+
+
+def test_spmv_api_edges(gpu):
+    A = P.CsrMatrix(3, 3, [0, 0, 0, 0], [], [])
+    assert np.array_equal(P.spmv(A, np.ones(3)), np.zeros(3))
+    with pytest.raises(ValueError, match="dimension mismatch"):
+        P.spmv(P.CsrMatrix.identity(3), np.ones(4))
+    assert P.dot(np.array([1.0, 0.0]), np.array([0.0, 1.0])) == 0.0
+    assert P.norm2(np.array([3.0, 4.0])) == 5.0
+    assert np.array_equal(P.axpy(2.0, np.array([1.0, 1.0]), np.array([1.0, 0.0])), [3.0, 2.0])
+    import torch
+    x = torch.arange(3, dtype=torch.float64, device="cuda")
+    y = P.spmv(P.CsrMatrix.identity(3), x)
+    assert y.is_cuda and torch.equal(y, x)
+
+
+def test_dot_deterministic(gpu):
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal(3_366_000)
+    y = rng.standard_normal(3_366_000)
+    d = P.dot(x, y)
+    assert all(P.dot(x, y) == d for _ in range(3))
+    assert abs(d - float(np.dot(x, y))) <= 1e-12 * np.abs(x * y).sum()
+
+
+# -- K4: PGS-SCM sweeps ---------------------------------------------------------
+
+
+def test_pgs_scm_sweep_bitwise(gpu):
+    g = load_golden("random_scalar.npz")
+    for ci in range(int(g["ncases"])):
+        p = f"c{ci}_"
+        n = g[p + "ptr"].shape[0] - 1
+        A = P.CsrMatrix(n, n, g[p + "ptr"], g[p + "cols"], g[p + "vals"])
+        part = P.vertices_grouping(P.strong_connections(A, float(g[p + "theta"])))
+        got = P.pgs_scm_sweep(A, g[p + "b"], g[p + "x0"], part)
+        assert np.array_equal(got, g[p + "sweep"]), ci
+
+
+def test_gs_kats(gpu):
+    A = P.CsrMatrix.from_dense([[2.0, -1.0], [-1.0, 2.0]])
+    assert np.array_equal(P.gs_sweep(A, np.ones(2), np.zeros(2)), [0.5, 0.75])
+    T = _csr(tridiag(4))
+    part = P.vertices_grouping(P.strong_connections(T, 1.0))
+    assert part.c == 1
+    assert np.array_equal(P.pgs_scm_sweep(T, np.ones(4), np.zeros(4), part),
+                          [0.5, 0.75, 0.875, 0.9375])
+    rng = np.random.default_rng(99)
+    for _ in range(8):
+        n = int(rng.integers(5, 120))
+        M = random_sparse(rng, n, avg_nnz=5, symmetric=bool(rng.integers(0, 2)))
+        for theta in (0.0, 0.3):
+            groups = orc.vertices_grouping(orc.strong_connections(M, theta))
+            part = P.ColorPartition.from_groups(groups, n)
+            b = rng.standard_normal(n)
+            x0 = rng.standard_normal(n)
+            ref = orc.ScmSmoother(M, groups)
+            for d in ("forward", "backward", "symmetric"):
+                got = P.PgsScmSmoother(_csr(M), part).apply(b, x0, direction=d)
+                assert np.array_equal(got, ref.apply(b, x0, direction=d)), (n, theta, d)
+
+
+# -- K8: BILU(0) solves ---------------------------------------------------------
+
+
+def test_bilu_apply_bitwise_given_factors(gpu):
+    rng = np.random.default_rng(5)
+    A, _ = _c1()
+    cases = [A] + [_bsr(random_block(rng, int(rng.integers(2, 150)), 3,
+                                     int(rng.integers(2, 7)))) for _ in range(6)]
+    cases += [_csr(random_sparse(rng, int(rng.integers(3, 300)), 6))]
+    for M in cases:
+        F = P.bilu0_factorize(M)
+        Fo = _oracle_bilu(F)
+        r = rng.standard_normal(Fo.n * Fo.b)
+        assert np.array_equal(P.bilu_apply(F, r), orc.bilu_apply(Fo, r))
+
+
+def test_bilu_apply_c1_vs_reference(gpu):
+    A, _ = _c1()
+    g = load_golden("c1_v0.npz")
+    F = P.bilu0_factorize(A)
+    np.testing.assert_allclose(P.bilu_apply(F, g["r_test"]), g["z_bilu"], rtol=1e-11, atol=1e-13)
+    with pytest.raises(ValueError, match="dimension mismatch"):
+        P.bilu_apply(F, np.ones(5))
+
+
+# -- AMG cycle + CPR apply ----------------------------------------------------------
+
+
+@pytest.mark.parametrize("tag", ["v0", "vd", "k0", "kd"])
+def test_amg_cycle_and_cpr_apply_c1(gpu, tag):
+    A, _ = _c1()
+    g = load_golden(f"c1_{tag}.npz")
+    B = P.build_cpr(A, P.SolverConfig(theta=0.0, theta_amg=0.0 if tag[1] == "0" else 0.08,
+                                      cycle=tag[0]))
+    zp = P.amg_cycle(B.pressure_solver, g["rp_test"])
+    np.testing.assert_allclose(zp, g["zp_cycle"], rtol=1e-10, atol=1e-12)
+    z = B.apply(g["r_test"])
+    np.testing.assert_allclose(z, g["z_apply"], rtol=1e-10, atol=1e-12)
+
+
+def test_vcycle_matches_oracle_with_same_coarse_solve(gpu):
+    A, _ = _c1()
+    B = P.build_cpr(A, P.SolverConfig(theta=0.0, theta_amg=0.0, cycle="v"))
+    Bo = orc.build_cpr(orc.Bsr(3, 1000, 1000, A.row_ptr, A.col_idx, A.values),
+                       orc.SolverConfig(theta=0.0, theta_amg=0.0, cycle="v"))
+    inv = B.pressure_solver.coarsest_lu[1]
+    rng = np.random.default_rng(3)
+    r = rng.standard_normal(1000)
+    zo = orc.amg_cycle(Bo.hierarchy, r, coarse_solve=lambda b: inv @ b)
+    np.testing.assert_allclose(P.amg_cycle(B.pressure_solver, r), zo, rtol=1e-13, atol=1e-15)
+
+
+def test_cpr_product_form_identity(gpu):
+    """Eq. 8 (tests/test_cpr.py:98-118): I - B A = (I - R A)(I - Pi B_P Pi^T A)."""
+    rng = np.random.default_rng(20240817)
+    for A in (_bsr(random_block(rng, 12, b=3)), _csr(random_sparse(rng, 40, avg_nnz=5))):
+        cfg = P.SolverConfig(coarsest_size=40, cycle="v", tol=1e-8, m=30)
+        B = P.build_cpr(A, cfg)
+        n = B.projector.fine_size
+        Ad = A.to_dense()
+
+        def assemble(op, size):
+            M = np.zeros((size, size))
+            for j in range(size):
+                e = np.zeros(size)
+                e[j] = 1.0
+                M[:, j] = op(e)
+            return M
+
+        Bm = assemble(B.apply, n)
+        Rm = assemble(lambda v: P.bilu_apply(B.relaxation, v), n)
+        idx = B.projector.pressure_indices
+        Pi = np.zeros((n, idx.shape[0]))
+        Pi[idx, np.arange(idx.shape[0])] = 1.0
+        BP = assemble(lambda v: P.amg_cycle(B.pressure_solver, v), idx.shape[0])
+        lhs = np.eye(n) - Bm @ Ad
+        rhs = (np.eye(n) - Rm @ Ad) @ (np.eye(n) - Pi @ BP @ Pi.T @ Ad)
+        assert np.abs(lhs - rhs).max() <= 1e-10
+
+
+# -- GMRES ------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("tag", ["v0", "k0", "vd", "kd"])
+def test_gmres_c1_against_reference(gpu, tag):
+    A, b = _c1()
+    g = load_golden(f"c1_{tag}.npz")
+    cfg = P.SolverConfig(theta=0.0, theta_amg=0.0 if tag[1] == "0" else 0.08, cycle=tag[0])
+    B = P.build_cpr(A, cfg)
+    res = P.gmres_solve(A, b, None, B, cfg.gmres_params(), history=True)
+    s = SUMMARY[tag]
+    assert (res.outer, res.inner, res.converged) == (s["outer"], s["inner"], s["converged"])
+    assert abs(res.rel_residual - s["rel"]) <= 1e-8 * s["rel"]
+    hist = np.array([h if not isinstance(h, tuple) else -h[1] for h in res.history])
+    np.testing.assert_allclose(hist, g["hist"], rtol=1e-8)
+    assert np.linalg.norm(res.x - g["x"]) <= 1e-9 * np.linalg.norm(g["x"])
+
+
+def test_gmres_kats(gpu):
+    A = P.CsrMatrix.identity(9)
+    b = np.linspace(1, 2, 9)
+    res = P.gmres_solve(A, b, None, None, P.GmresParams(m=5, tol=1e-10))
+    assert res.converged and res.outer == 1 and np.allclose(res.x, b, atol=1e-14)
+    A = P.CsrMatrix.from_dense(np.diag(np.arange(1.0, 11.0)))
+    res = P.gmres_solve(A, np.ones(10), None, None, P.GmresParams(m=10, tol=1e-5))
+    assert res.converged and res.outer == 1
+    assert np.linalg.norm(res.x - 1.0 / np.arange(1.0, 11.0)) <= 1e-8
+    A = P.CsrMatrix.from_dense(np.diag([3.0, 5.0, 7.0]))
+    res = P.gmres_solve(A, np.array([0.0, 2.0, 0.0]), None, None, P.GmresParams(m=5, tol=1e-12))
+    assert res.converged and res.inner == 1 and np.allclose(res.x, [0.0, 0.4, 0.0], atol=1e-14)
+    rng = np.random.default_rng(1)
+    M = _csr(random_sparse(rng, 8))
+    res = P.gmres_solve(M, np.zeros(8), None, None)
+    assert res.converged and res.outer == 0 and res.inner == 0
+    Pm = _csr(poisson_2d(10, 10))
+    res = P.gmres_solve(Pm, rng.standard_normal(100), None, None,
+                        P.GmresParams(m=2, max_restarts=3, tol=1e-14))
+    assert not res.converged and res.outer == 3
+    D = P.CsrMatrix.from_dense([[1e308, 0.0], [0.0, 1e308]])
+    with pytest.raises(FloatingPointError):
+        P.gmres_solve(D, np.array([1e308, 1e308]), np.array([1e308, 1e308]), None)
+
+
+def test_gmres_matches_oracle_unpreconditioned(gpu):
+    rng = np.random.default_rng(1234)
+    for _ in range(6):
+        n = int(rng.integers(5, 120))
+        M = random_sparse(rng, n, avg_nnz=6)
+        xs = rng.standard_normal(n)
+        b = orc.spmv(M, xs)
+        res = P.gmres_solve(_csr(M), b, None, None, P.GmresParams(m=30, max_restarts=400, tol=1e-8))
+        ro = orc.gmres_solve(M, b, None, None, 30, 400, 1e-8)
+        assert (res.outer, res.inner) == (ro.outer, ro.inner)
+        assert np.linalg.norm(res.x - ro.x) <= 1e-9 * np.linalg.norm(ro.x)
+
+
+def test_poisson32_vcycle_acceptance(gpu):
+    A = _csr(poisson_2d(32, 32))
+    h = P.build_hierarchy(A, P.AmgParams(coarsest_size=256, cycle="v"))
+    b = np.ones(A.nrows)
+    x = np.zeros(A.nrows)
+    res = SUMMARY["poisson32"]["res"]
+    for k in range(25):
+        x = x + P.amg_cycle(h, b - P.spmv(A, x))
+        assert abs(np.linalg.norm(b - P.spmv(A, x)) - res[k]) <= 1e-8 * res[k]
+    assert np.linalg.norm(b) / res[-1] >= 1e6
+
+
+def test_pressure16_vcycle(gpu):
+    s = SUMMARY["press16"]
+    A = P.problems.pressure_operator(16, 16, 16)
+    h = P.build_hierarchy(A, P.AmgParams(theta_amg=0.0, cycle="v"))
+    b = np.ones(A.nrows)
+    x = np.zeros(A.nrows)
+    for k in range(6):
+        x = x + P.amg_cycle(h, b - P.spmv(A, x))
+        rel = np.linalg.norm(b - P.spmv(A, x)) / np.linalg.norm(b)
+        assert abs(rel - s["rel"][k]) <= 1e-9 * s["rel"][k]
+
+
+def test_acceptance_sequence_iter50(gpu):
+    """pkg/test_output.txt:203 (Iter=50, SetupCalls=1 on 32x32x4x10, mu=15)."""
+    s = SUMMARY["accept_seq"]
+    seq = P.generate_blackoil_like_sequence(32, 32, 4, 10, 0.01, seed=20240817)
+    cfg = P.SolverConfig(theta=0.0, mu=15, m=28, tol=1e-5, cycle="v", coarsest_size=200)
+    out = P.ascpr_gmres_sequence(seq.systems, 15, cfg)
+    assert out.setup_calls == s["setup_calls"] and out.total_inner == s["total_inner"]
+    assert [r.rebuilt for r in out.records] == s["rebuilt"]
+    np.testing.assert_allclose([r.rel_residual for r in out.records], s["rel"], rtol=1e-8)
+
+
+def test_ascpr_rules(gpu):
+    rng = np.random.default_rng(7)
+    A = _bsr(random_block(rng, 20, b=3))
+    systems = [(A, P.spmv(A, rng.standard_normal(60))) for _ in range(4)]
+    for mu, calls in ((0, 4), (10_000, 1)):
+        out = P.ascpr_gmres_sequence(systems, mu=mu,
+                                     config=P.SolverConfig(coarsest_size=40, cycle="v", tol=1e-9))
+        assert out.setup_calls == calls and out.all_converged
+        for (Ak, bk), rec in zip(systems, out.records):
+            assert np.linalg.norm(bk - P.spmv(Ak, rec.x)) <= 1e-8 * np.linalg.norm(bk)
+
+
+@pytest.mark.slow
+def test_spe10_shape_c3_against_reference(gpu):
+    """Config 3 (60x220x85, 3,366,000 DOF), theta_amg = 0, V-cycle: the
+    reference's iteration counts, Givens history (1e-8) and solution (1e-6)."""
+    path = GOLDEN / "c3_v0.json"
+    if not path.exists():
+        pytest.skip("c3 fixture not generated")
+    ref = json.loads(path.read_text())
+    (A, b), = P.generate_blackoil_like_sequence(60, 220, 85, 1, 0.01, 0).systems
+    cfg = P.SolverConfig(theta=0.0, theta_amg=0.0, cycle="v")
+    B = P.build_cpr(A, cfg)
+    h = B.pressure_solver
+    assert [l.A.nrows for l in h.levels] == ref["sizes"]
+    assert [l.partition.c if l.partition else None for l in h.levels] == ref["colors"]
+    res = P.gmres_solve(A, b, None, B, cfg.gmres_params(), history=True)
+    assert (res.outer, res.inner) == (ref["outer"], ref["inner"])
+    hist = np.array([hh if not isinstance(hh, tuple) else -hh[1] for hh in res.history])
+    np.testing.assert_allclose(hist, ref["hist"], rtol=1e-8)
+    xs = np.asarray(ref["x_sample"])
+    got = res.x[::ref["x_sample_stride"]]
+    assert np.linalg.norm(got - xs) <= 1e-6 * np.linalg.norm(xs)
+    assert abs(np.linalg.norm(res.x) - ref["x_norm"]) <= 1e-6 * ref["x_norm"]
