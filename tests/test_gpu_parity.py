@@ -280,7 +280,9 @@ def test_poisson32_vcycle_acceptance(gpu):
     res = SUMMARY["poisson32"]["res"]
     for k in range(25):
         x = x + P.amg_cycle(h, b - P.spmv(A, x))
-        assert abs(np.linalg.norm(b - P.spmv(A, x)) - res[k]) <= 1e-8 * res[k]
+        # late cycles: |r| ~ 1e-7 |b|, so rounding of the coarse solve (dense
+        # inverse vs the reference's LU) shows at ~1e-14 |b|
+        assert abs(np.linalg.norm(b - P.spmv(A, x)) - res[k]) <= 1e-8 * res[k] + 1e-13 * 32.0
     assert np.linalg.norm(b) / res[-1] >= 1e6
 
 
