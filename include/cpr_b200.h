@@ -139,13 +139,43 @@ typedef struct cprb_amg {
   int64_t kwork_len;
 } cprb_amg;
 
+/* Chunked-wavefront plan of one triangular factor (csrc/wave.cu).  Rows are
+ * cut into contiguous chunks of one dependency bandwidth; inside a chunk rows
+ * are grouped into level "steps" (<= 64 rows).  Each step is one contiguous,
+ * 16-byte aligned block of `stream`:
+ *   int32 rows[Wp], lens[Wp], aux[Wp], codes[K][Wp];
+ *   f64 vals[K][b*b][Wp]; (upper factor) f64 uinv[b*b][Wp]
+ * with Wp = round_up(w, 4); a code < 0 names a shared-memory ring slot
+ * (-code-1), otherwise the dependency's row.  The step's right-hand side is
+ * rhs[rhs_off[k] ...] (w*b doubles, 16-byte aligned). */
+typedef struct cprb_wave {
+  int32_t nchunks;
+  int32_t nsteps;
+  int32_t stage_max;           /* max step_bytes (multiple of 16) */
+  int32_t rhs_max;             /* max rhs_bytes (multiple of 16) */
+  const int32_t* chunk_step;   /* dev, nchunks+1 */
+  const int64_t* step_off;     /* dev, byte offsets into stream */
+  const int32_t* step_bytes;   /* dev */
+  const int32_t* step_w;       /* dev */
+  const int32_t* step_k;       /* dev */
+  const int64_t* rhs_off;      /* dev, double offsets into the rhs vector */
+  const int32_t* rhs_bytes;    /* dev */
+  const uint8_t* stream;       /* dev */
+} cprb_wave;
+
 typedef struct cprb_bilu {
   int32_t n;                   /* block rows */
   int32_t b;                   /* block size (1 or 3) */
   cprb_sell L;                 /* strict lower blocks; lanes in L-level order */
   cprb_sell U;                 /* strict upper blocks; lanes in U-level order */
   const double* uinv;          /* dev, U lane layout: [(s*b*b + e)*32 + l] */
-  int32_t* tickets;            /* dev, 2 ints (dynamic warp ordering) */
+  int32_t* tickets;            /* dev, 4 ints (dynamic warp / chunk ordering) */
+  int32_t use_wave;            /* 1: chunked-wavefront kernels (Lw/Uw) */
+  cprb_wave Lw;
+  cprb_wave Uw;
+  const int32_t* l_slot;       /* dev, n: rhs slot of each row in the L plan */
+  double* rhs_l;               /* dev work: rhs in L step order */
+  double* rhs_u;               /* dev work: z in U step order */
 } cprb_bilu;
 
 typedef struct cprb_cpr {
@@ -191,6 +221,10 @@ int cprb_bilu_apply(const cprb_bilu* F, const double* r, double* z, double* work
 
 /* src/cpr.py:178-186  z = B r (V-cycle pressure stage). */
 int cprb_cpr_apply(const cprb_cpr* P, const double* r, double* z, void* stream);
+/* Graph-replayed cprb_cpr_apply: one cached CUDA graph per (P, r, z). */
+int cprb_graph_cache_create(void** out);
+int cprb_graph_cache_destroy(void* cache);
+int cprb_cpr_apply_graph(void* cache, const cprb_cpr* P, const double* r, double* z, void* stream);
 /* src/cpr.py:184-186  second half given zp already in P->zp. */
 int cprb_cpr_finish(const cprb_cpr* P, const double* r, double* z, void* stream);
 

@@ -45,9 +45,17 @@ class Amg(C.Structure):
                 ("kwork", vp), ("kwork_len", C.c_int64)]
 
 
+class Wave(C.Structure):
+    _fields_ = [("nchunks", C.c_int32), ("nsteps", C.c_int32), ("stage_max", C.c_int32),
+                ("rhs_max", C.c_int32), ("chunk_step", vp), ("step_off", vp), ("step_bytes", vp),
+                ("step_w", vp), ("step_k", vp), ("rhs_off", vp), ("rhs_bytes", vp),
+                ("stream", vp)]
+
+
 class Bilu(C.Structure):
     _fields_ = [("n", C.c_int32), ("b", C.c_int32), ("L", Sell), ("U", Sell), ("uinv", vp),
-                ("tickets", vp)]
+                ("tickets", vp), ("use_wave", C.c_int32), ("Lw", Wave), ("Uw", Wave),
+                ("l_slot", vp), ("rhs_l", vp), ("rhs_u", vp)]
 
 
 class Cpr(C.Structure):
@@ -77,6 +85,9 @@ _SIGS = {
     "cprb_coarse_solve": (C.c_int, [C.POINTER(Amg), vp, vp, vp]),
     "cprb_resid_restrict": (C.c_int, [C.POINTER(AmgLevel), vp, vp, vp, vp]),
     "cprb_prolong": (C.c_int, [C.POINTER(AmgLevel), vp, vp, vp]),
+    "cprb_graph_cache_create": (C.c_int, [C.POINTER(C.c_void_p)]),
+    "cprb_graph_cache_destroy": (C.c_int, [vp]),
+    "cprb_cpr_apply_graph": (C.c_int, [vp, C.POINTER(Cpr), vp, vp, vp]),
     "cprb_cpr_finish": (C.c_int, [C.POINTER(Cpr), vp, vp, vp]),
     "cprb_div_host": (C.c_int, [C.c_int64, vp, C.c_double, vp, vp]),
     "cprb_dot": (C.c_int, [C.c_int64, vp, vp, vp, vp, vp, vp]),

@@ -184,5 +184,10 @@ extern "C" int cprb_bilu_apply(const cprb_bilu* F, const double* r, double* z, d
   if (n == 0) return CPRB_OK;
   int rc = fill_sentinel(work_l, n, st);
   if (rc) return rc;
+  if (F->use_wave) {
+    rc = wave_scatter_rhs(*F, r, F->rhs_l, st);
+    if (rc) return rc;
+    return wave_solve(*F, F->rhs_l, work_l, F->rhs_u, z, nullptr, nullptr, st);
+  }
   return bilu_solve(*F, r, work_l, z, nullptr, nullptr, st);
 }

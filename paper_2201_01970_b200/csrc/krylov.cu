@@ -225,6 +225,13 @@ int cprb_div_scalar(int64_t n, const double* x, const double* h_dev, double* out
 // src/cpr.py:184-186 given zp in P->zp:  r2 = r - A Pi zp;  z = Pi zp + BILU(r2)
 int cprb_cpr_finish(const cprb_cpr* P, const double* r, double* z, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
+  const cprb_bilu& F = P->bilu;
+  if (F.use_wave) {
+    // stage-2 residual written straight into the L plan's step order
+    int rc = bsr_op(2, P->A, P->b, P->zp, r, F.rhs_l, nullptr, P->zl, st, F.l_slot);
+    if (rc) return rc;
+    return wave_solve(F, F.rhs_l, P->zl, F.rhs_u, P->y, P->zp, z, st);
+  }
   int rc = bsr_op(2, P->A, P->b, P->zp, r, P->r2, nullptr, P->zl, st);  // also arms zl
   if (rc) return rc;
   return bilu_solve(P->bilu, P->r2, P->zl, P->y, P->zp, z, st);

@@ -69,7 +69,8 @@ template <int B, int MODE>
 __global__ void __launch_bounds__(256) k_bsr(const cprb_sell A, const double* __restrict__ x,
                                              const double* __restrict__ rhs,
                                              double* __restrict__ out, int32_t* flag,
-                                             double* __restrict__ sent) {
+                                             double* __restrict__ sent,
+                                             const int32_t* __restrict__ out_idx) {
   const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (w >= A.nslices) return;
@@ -94,11 +95,12 @@ __global__ void __launch_bounds__(256) k_bsr(const cprb_sell A, const double* __
     default: bsr_row_generic<B, MODE>(A, base, lane, len, x, res); break;
   }
   bool bad = false;
+  const int64_t ob = out_idx ? (int64_t)out_idx[row] : (int64_t)B * row;
 #pragma unroll
   for (int r = 0; r < B; ++r) {
     const int64_t o = (int64_t)B * row + r;
     const double v = (MODE == 0) ? res[r] : rhs[o] - res[r];
-    out[o] = v;
+    out[ob + r] = v;
     bad |= !isfinite(v);
     if (MODE == 2 && sent) sent[o] = sentinel();
   }
@@ -107,23 +109,23 @@ __global__ void __launch_bounds__(256) k_bsr(const cprb_sell A, const double* __
 
 template <int B, int MODE>
 static void launch_bsr(const cprb_sell& A, const double* x, const double* rhs, double* out,
-                       int32_t* flag, double* sent, cudaStream_t st) {
+                       int32_t* flag, double* sent, cudaStream_t st, const int32_t* oi) {
   if (A.nslices <= 0) return;
   const int threads = 256;
   const int blocks = (A.nslices * 32 + threads - 1) / threads;
-  k_bsr<B, MODE><<<blocks, threads, 0, st>>>(A, x, rhs, out, flag, sent);
+  k_bsr<B, MODE><<<blocks, threads, 0, st>>>(A, x, rhs, out, flag, sent, oi);
 }
 
 int bsr_op(int mode, const cprb_sell& A, int b, const double* x, const double* rhs, double* out,
-           int32_t* flag, double* sent, cudaStream_t st) {
+           int32_t* flag, double* sent, cudaStream_t st, const int32_t* oi) {
   if (b == 3) {
-    if (mode == 0) launch_bsr<3, 0>(A, x, rhs, out, flag, sent, st);
-    else if (mode == 1) launch_bsr<3, 1>(A, x, rhs, out, flag, sent, st);
-    else launch_bsr<3, 2>(A, x, rhs, out, flag, sent, st);
+    if (mode == 0) launch_bsr<3, 0>(A, x, rhs, out, flag, sent, st, oi);
+    else if (mode == 1) launch_bsr<3, 1>(A, x, rhs, out, flag, sent, st, oi);
+    else launch_bsr<3, 2>(A, x, rhs, out, flag, sent, st, oi);
   } else if (b == 1) {
-    if (mode == 0) launch_bsr<1, 0>(A, x, rhs, out, flag, sent, st);
-    else if (mode == 1) launch_bsr<1, 1>(A, x, rhs, out, flag, sent, st);
-    else launch_bsr<1, 2>(A, x, rhs, out, flag, sent, st);
+    if (mode == 0) launch_bsr<1, 0>(A, x, rhs, out, flag, sent, st, oi);
+    else if (mode == 1) launch_bsr<1, 1>(A, x, rhs, out, flag, sent, st, oi);
+    else launch_bsr<1, 2>(A, x, rhs, out, flag, sent, st, oi);
   } else {
     return set_error(CPRB_EUNSUPPORTED, "block size " + std::to_string(b) + " not supported on device");
   }

@@ -1,0 +1,289 @@
+// K8 (fast path): chunked-wavefront BILU(0) triangular solves.
+//
+// Rows are split into contiguous chunks whose length is the dependency
+// bandwidth of the factor (one xy-plane for the natural-ordered 7-point
+// grid), so a chunk only depends on the chunk before it (L) / after it (U).
+// One persistent CTA owns a chunk at a time (ticket order = dependency order,
+// so waiting is deadlock free) and walks its rows level by level ("steps",
+// <= 64 rows, one row per thread):
+//   * the step's blocks, column codes and right-hand side arrive in shared
+//     memory through cp.async.bulk (TMA) copies issued DEPTH steps ahead on
+//     mbarriers, so HBM latency is off the critical path;
+//   * a dependency inside the chunk that is < RING steps old is read from a
+//     shared-memory ring; anything else is polled from global memory, where
+//     every result is published with a relaxed store (sentinel = not ready);
+//   * the rest is a __syncthreads per step.
+// The critical path is ~(#levels x smem step) + (#chunks x one L2 hop)
+// instead of #levels x L2 hops.  Arithmetic is the reference's: einsum block
+// products ((p0 + p2) + p1), reduceat row sums (src/ilu.py:97-107, :216-222).
+#include "device.cuh"
+#include "engine.h"
+
+namespace cprb {
+
+constexpr int WAVE_THREADS = 64;  // == wmax of the plan
+constexpr int WAVE_DEPTH = 6;
+constexpr int WAVE_RING = 4;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+struct WaveSmem {
+  uint8_t* stage;     // DEPTH * stage_max
+  double* rhs;        // DEPTH * rhs_max/8
+  double* ring;       // RING * WAVE_THREADS * B
+  uint64_t* bar;      // DEPTH
+  int* chunk;         // 1
+};
+
+template <int B, int K, bool UPPER>
+__device__ __forceinline__ void wave_rowsum_fixed(const int32_t* codes, const double* vals, int Wp,
+                                                  int t, const double* ring, const double* glob,
+                                                  double* tsum) {
+  double v[K][B];
+#pragma unroll
+  for (int m = 0; m < K; ++m) {
+    const int code = codes[m * Wp + t];
+    if (code < 0) {
+      const double* s = ring + (int64_t)(-code - 1) * B;
+#pragma unroll
+      for (int c = 0; c < B; ++c) v[m][c] = s[c];
+    } else {
+#pragma unroll
+      for (int c = 0; c < B; ++c) v[m][c] = wait_value(glob + (int64_t)B * code + c);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < B; ++r) {
+    double p[K];
+#pragma unroll
+    for (int m = 0; m < K; ++m) {
+      double mr[B];
+#pragma unroll
+      for (int c = 0; c < B; ++c) mr[c] = vals[(int64_t)(m * B * B + r * B + c) * Wp + t];
+      p[m] = block_row_dot<B>(mr, v[m]);
+    }
+    tsum[r] = segsum_fixed<K>(p);
+  }
+}
+
+template <int B>
+__device__ __forceinline__ void wave_rowsum_generic(const int32_t* codes, const double* vals,
+                                                    int Wp, int t, int len, const double* ring,
+                                                    const double* glob, double* tsum) {
+#pragma unroll
+  for (int r = 0; r < B; ++r) {
+    auto f = [&](int m) -> double {
+      const int code = codes[m * Wp + t];
+      double v[B], mr[B];
+#pragma unroll
+      for (int c = 0; c < B; ++c) {
+        v[c] = code < 0 ? ring[(int64_t)(-code - 1) * B + c] : wait_value(glob + (int64_t)B * code + c);
+        mr[c] = vals[(int64_t)(m * B * B + r * B + c) * Wp + t];
+      }
+      return block_row_dot<B>(mr, v);
+    };
+    tsum[r] = segsum_rt(f, len);
+  }
+}
+
+// UPPER = false: z = r - sum L z   (publishes z, copies z into the U plan's
+//                rhs order via aux slots, arms y with the sentinel)
+// UPPER = true : y = Uinv (z - sum U y); final = z1 + y
+template <int B, bool UPPER>
+__global__ void __launch_bounds__(WAVE_THREADS, 1)
+    k_wave(const cprb_wave W, const double* __restrict__ rhs_steps, double* out_nat,
+           double* __restrict__ next_rhs, double* __restrict__ arm, const double* __restrict__ zp,
+           double* __restrict__ final_out, int32_t* ticket) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  constexpr int BB = B * B;
+  const int tid = threadIdx.x;
+  const int stage_max = W.stage_max, rhs_max = W.rhs_max;
+  WaveSmem S;
+  S.stage = smem_raw;
+  S.rhs = reinterpret_cast<double*>(smem_raw + (size_t)WAVE_DEPTH * stage_max);
+  S.ring = S.rhs + (size_t)WAVE_DEPTH * (rhs_max / 8);
+  S.bar = reinterpret_cast<uint64_t*>(S.ring + (size_t)WAVE_RING * WAVE_THREADS * B);
+  S.chunk = reinterpret_cast<int*>(S.bar + WAVE_DEPTH);
+  if (tid == 0) {
+    for (int d = 0; d < WAVE_DEPTH; ++d) mbar_init(&S.bar[d], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t g = 0;  // steps consumed by this CTA (stage = g % DEPTH, parity = (g / DEPTH) & 1)
+
+  auto issue = [&](int k, uint32_t gg) {
+    const int st = gg % WAVE_DEPTH;
+    const uint32_t sb = W.step_bytes[k];
+    const uint32_t rb = W.rhs_bytes[k];
+    mbar_expect_tx(&S.bar[st], sb + rb);
+    bulk_g2s(S.stage + (size_t)st * stage_max, W.stream + W.step_off[k], sb, &S.bar[st]);
+    bulk_g2s(S.rhs + (size_t)st * (rhs_max / 8), rhs_steps + W.rhs_off[k], rb, &S.bar[st]);
+  };
+
+  while (true) {
+    if (tid == 0) {
+      const int c = atomicAdd(ticket, 1);
+      if (c == W.nchunks + (int)gridDim.x - 1) atomicExch(ticket, 0);
+      *S.chunk = c;
+    }
+    __syncthreads();
+    const int c = *S.chunk;
+    __syncthreads();
+    if (c >= W.nchunks) break;
+    const int s0 = W.chunk_step[c], s1 = W.chunk_step[c + 1];
+    if (tid == 0)
+      for (int k = s0; k < s1 && k < s0 + WAVE_DEPTH; ++k) issue(k, g + (k - s0));
+    for (int k = s0; k < s1; ++k, ++g) {
+      const int st = g % WAVE_DEPTH;
+      mbar_wait(&S.bar[st], (g / WAVE_DEPTH) & 1);
+      const uint8_t* blk = S.stage + (size_t)st * stage_max;
+      const int w = W.step_w[k], K = W.step_k[k];
+      const int Wp = (w + 3) & ~3;
+      const int32_t* rows = reinterpret_cast<const int32_t*>(blk);
+      const int32_t* lens = rows + Wp;
+      const int32_t* aux = lens + Wp;
+      const int32_t* codes = aux + Wp;
+      const double* vals = reinterpret_cast<const double*>(blk + (size_t)(12 + 4 * K) * Wp);
+      const double* uinv = vals + (size_t)K * BB * Wp;
+      const double* rhs = S.rhs + (size_t)st * (rhs_max / 8);
+      if (tid < w) {
+        const int row = rows[tid];
+        const int len = lens[tid];
+        double z1 = 0.0;
+        if (UPPER && zp) z1 = zp[row];
+        double ts[B];
+        switch (len) {
+          case 0:
+#pragma unroll
+            for (int r = 0; r < B; ++r) ts[r] = 0.0;
+            break;
+          case 1: wave_rowsum_fixed<B, 1, UPPER>(codes, vals, Wp, tid, S.ring, out_nat, ts); break;
+          case 2: wave_rowsum_fixed<B, 2, UPPER>(codes, vals, Wp, tid, S.ring, out_nat, ts); break;
+          case 3: wave_rowsum_fixed<B, 3, UPPER>(codes, vals, Wp, tid, S.ring, out_nat, ts); break;
+          default: wave_rowsum_generic<B>(codes, vals, Wp, tid, len, S.ring, out_nat, ts); break;
+        }
+        double res[B];
+        if constexpr (!UPPER) {
+#pragma unroll
+          for (int r = 0; r < B; ++r) res[r] = rhs[tid * B + r] - ts[r];
+        } else {
+          double d[B], ui[BB];
+#pragma unroll
+          for (int r = 0; r < B; ++r) d[r] = rhs[tid * B + r] - ts[r];
+#pragma unroll
+          for (int e = 0; e < BB; ++e) ui[e] = uinv[(size_t)e * Wp + tid];
+#pragma unroll
+          for (int r = 0; r < B; ++r) res[r] = block_row_dot<B>(&ui[r * B], d);
+        }
+        double* ring_slot = S.ring + ((size_t)(k % WAVE_RING) * WAVE_THREADS + tid) * B;
+#pragma unroll
+        for (int r = 0; r < B; ++r) {
+          ring_slot[r] = res[r];
+          st_relaxed(out_nat + (int64_t)B * row + r, res[r]);
+        }
+        if constexpr (!UPPER) {
+          const int ns = aux[tid];
+#pragma unroll
+          for (int r = 0; r < B; ++r) {
+            next_rhs[(int64_t)ns + r] = res[r];
+            arm[(int64_t)B * row + r] = sentinel();
+          }
+        } else {
+          if (final_out) {
+#pragma unroll
+            for (int r = 0; r < B; ++r)
+              final_out[(int64_t)B * row + r] = zp ? ((r == 0 ? z1 : 0.0) + res[r]) : res[r];
+          }
+        }
+      }
+      __syncthreads();  // ring + stage buffer reuse
+      if (tid == 0 && k + WAVE_DEPTH < s1) issue(k + WAVE_DEPTH, g + WAVE_DEPTH);
+    }
+  }
+}
+
+// scatter r into the L plan's step order (slots) for standalone applies
+__global__ void k_scatter_slots(int n, int b, const int32_t* __restrict__ slot,
+                                const double* __restrict__ r, double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int c = 0; c < b; ++c) out[slot[i] + c] = r[(int64_t)b * i + c];
+}
+
+static size_t wave_smem(const cprb_wave& W, int b) {
+  return (size_t)WAVE_DEPTH * (W.stage_max + W.rhs_max) + (size_t)WAVE_RING * WAVE_THREADS * b * 8 +
+         WAVE_DEPTH * 8 + 16;
+}
+
+template <int B, bool UPPER>
+static int launch_wave(const cprb_wave& W, const double* rhs_steps, double* out_nat, double* next_rhs,
+                       double* arm, const double* zp, double* final_out, int32_t* ticket,
+                       cudaStream_t st) {
+  static int num_sms = 0;
+  if (!num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const size_t smem = wave_smem(W, B);
+  cudaFuncSetAttribute(k_wave<B, UPPER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int grid = W.nchunks < num_sms ? W.nchunks : num_sms;
+  k_wave<B, UPPER><<<grid, WAVE_THREADS, smem, st>>>(W, rhs_steps, out_nat, next_rhs, arm, zp,
+                                                     final_out, ticket);
+  return check_launch("wave solve");
+}
+
+// L then U; rhsL: r in L-step order; zl: natural z (sentinel-armed by caller);
+// zu_rhs: z in U-step order (written by L); y: natural y; zout = Pi zp + y.
+int wave_solve(const cprb_bilu& F, const double* rhsL, double* zl, double* zu_rhs, double* y,
+               const double* zp, double* zout, cudaStream_t st) {
+  int rc;
+  if (F.b == 3) {
+    rc = launch_wave<3, false>(F.Lw, rhsL, zl, zu_rhs, y, nullptr, nullptr, F.tickets + 2, st);
+    if (rc) return rc;
+    rc = launch_wave<3, true>(F.Uw, zu_rhs, y, nullptr, nullptr, zp, zout, F.tickets + 3, st);
+  } else if (F.b == 1) {
+    rc = launch_wave<1, false>(F.Lw, rhsL, zl, zu_rhs, y, nullptr, nullptr, F.tickets + 2, st);
+    if (rc) return rc;
+    rc = launch_wave<1, true>(F.Uw, zu_rhs, y, nullptr, nullptr, zp, zout, F.tickets + 3, st);
+  } else {
+    return set_error(CPRB_EUNSUPPORTED, "wave BILU supports block sizes 1 and 3");
+  }
+  return rc;
+}
+
+int wave_scatter_rhs(const cprb_bilu& F, const double* r, double* rhsL, cudaStream_t st) {
+  k_scatter_slots<<<(F.n + 255) / 256, 256, 0, st>>>(F.n, F.b, F.l_slot, r, rhsL);
+  return check_launch("scatter slots");
+}
+
+}  // namespace cprb

@@ -66,9 +66,9 @@ class BiluFactors:
     def n(self) -> int:
         return self.L.nrows
 
-    def device(self) -> "DeviceBilu":
-        if self._dev is None:
-            self._dev = DeviceBilu(self)
+    def device(self, use_wave: bool = True) -> "DeviceBilu":
+        if self._dev is None or self._dev.use_wave != (use_wave and self.n > 0):
+            self._dev = DeviceBilu(self, use_wave)
         return self._dev
 
 
@@ -151,10 +151,121 @@ def _level_sell(T: BlockCsrMatrix, sched: LevelSchedule, b: int, uinv=None):
     return h, ui
 
 
+WAVE_WMAX = 64          # rows per step == threads per CTA (csrc/wave.cu)
+WAVE_RING = 4           # steps kept in the shared-memory ring
+WAVE_STAGE_CAP = 24576  # bytes per streamed step
+
+
+def _round16(x):
+    return (x + 15) // 16 * 16
+
+
+def wave_plan(T: BlockCsrMatrix, sched: LevelSchedule, b: int, upper: bool, uinv=None,
+              aux_slot=None, nchunk_min: int = 148):
+    """Chunked-wavefront plan of a strict triangular factor (see cprb_wave in
+    include/cpr_b200.h).  Returns (host arrays dict, row -> rhs slot)."""
+    ptr, cols, vals = _strict(T)
+    n = T.nrows
+    bb = b * b
+    vals = np.asarray(vals, dtype=np.float64).reshape(-1, bb)
+    lens = np.diff(ptr)
+    rows_of = np.repeat(np.arange(n, dtype=np.int64), lens)
+    level = np.zeros(n, dtype=np.int64)
+    for li, lv in enumerate(sched.levels):
+        level[lv] = li
+    bw = int(np.abs(rows_of - cols).max()) if cols.size else 1
+    R = max(bw, -(-n // nchunk_min), 1)
+    pos = (n - 1 - np.arange(n)) if upper else np.arange(n)
+    chunk = pos // R
+    order = np.lexsort((np.arange(n), level, chunk))     # rows by (chunk, level, index)
+    ch_s, lv_s = chunk[order], level[order]
+    newg = np.ones(n, dtype=bool)
+    newg[1:] = (np.diff(ch_s) != 0) | (np.diff(lv_s) != 0)
+    gstart = np.flatnonzero(newg)
+    gsize = np.diff(np.append(gstart, n))
+    gid = np.repeat(np.arange(gstart.shape[0]), gsize)
+    Kg = np.maximum.reduceat(lens[order], gstart) if n else np.zeros(0, np.int64)
+    row_bytes = 12 + 4 * Kg + 8 * Kg * bb + (8 * bb if upper else 0)
+    cap = np.minimum(WAVE_WMAX, np.maximum(1, (WAVE_STAGE_CAP - 64) // row_bytes))
+    nsub = -(-gsize // cap)
+    gstep0 = np.zeros(gstart.shape[0] + 1, dtype=np.int64)
+    np.cumsum(nsub, out=gstep0[1:])
+    pin = np.arange(n) - gstart[gid]
+    sub = pin // cap[gid]
+    step_of_sorted = gstep0[gid] + sub
+    p_sorted = pin - sub * cap[gid]
+    nsteps = int(gstep0[-1])
+    row_step = np.empty(n, dtype=np.int64)
+    row_pos = np.empty(n, dtype=np.int64)
+    row_step[order] = step_of_sorted
+    row_pos[order] = p_sorted
+    step_w = np.bincount(step_of_sorted, minlength=nsteps)
+    step_k = np.zeros(nsteps, dtype=np.int64)
+    np.maximum.at(step_k, step_of_sorted, lens[order])
+    step_chunk = np.zeros(nsteps, dtype=np.int64)
+    step_chunk[step_of_sorted] = ch_s
+    nchunks = int(chunk.max()) + 1 if n else 0
+    chunk_step = np.searchsorted(step_chunk, np.arange(nchunks + 1)).astype(np.int32)
+    Wp = (step_w + 3) // 4 * 4
+    sbytes = Wp * (12 + 4 * step_k) + 8 * step_k * bb * Wp + (8 * bb * Wp if upper else 0)
+    soff = np.zeros(nsteps + 1, dtype=np.int64)
+    np.cumsum(sbytes, out=soff[1:])
+    rbytes = np.array([_round16(int(w) * b * 8) for w in step_w], dtype=np.int64) \
+        if nsteps < 4096 else (step_w * b * 8 + 15) // 16 * 16
+    roff = np.zeros(nsteps + 1, dtype=np.int64)
+    np.cumsum(rbytes // 8, out=roff[1:])
+    stream = np.zeros(max(int(soff[-1]), 16), dtype=np.uint8)
+    I = stream.view(np.int32)
+    F = stream.view(np.float64)
+    st = row_step
+    base4 = soff[st] // 4
+    I[base4 + row_pos] = np.arange(n)                              # rows
+    I[base4 + Wp[st] + row_pos] = lens                              # lens
+    aux = np.zeros(n, dtype=np.int64) if aux_slot is None else aux_slot
+    I[base4 + 2 * Wp[st] + row_pos] = aux                           # aux (next rhs slot)
+    # entries
+    ent = np.arange(cols.shape[0], dtype=np.int64)
+    m = ent - ptr[rows_of]
+    ri = rows_of
+    dep = cols
+    internal = (chunk[dep] == chunk[ri]) & (row_step[ri] - row_step[dep] < WAVE_RING)
+    slot = (row_step[dep] % WAVE_RING) * WAVE_WMAX + row_pos[dep]
+    code = np.where(internal, -(slot + 1), dep)
+    e_st = row_step[ri]
+    e_Wp = Wp[e_st]
+    I[soff[e_st] // 4 + 3 * e_Wp + m * e_Wp + row_pos[ri]] = code
+    vbase = (soff[e_st] + (12 + 4 * step_k[e_st]) * e_Wp) // 8
+    e_idx = np.arange(bb, dtype=np.int64)
+    F[(vbase + (m * bb) * e_Wp + row_pos[ri])[:, None] + e_idx[None, :] * e_Wp[:, None]] = vals
+    if upper:
+        ub = (soff[st] + (12 + 4 * step_k[st]) * Wp[st] + 8 * step_k[st] * bb * Wp[st]) // 8
+        F[(ub + row_pos)[:, None] + e_idx[None, :] * Wp[st][:, None]] = \
+            np.asarray(uinv, dtype=np.float64).reshape(n, bb)
+    rhs_slot = roff[st] + row_pos * b
+    host = dict(nchunks=nchunks, nsteps=nsteps, stage_max=int(sbytes.max(initial=16)),
+                rhs_max=int(rbytes.max(initial=16)), chunk_step=chunk_step,
+                step_off=soff[:-1].astype(np.int64), step_bytes=sbytes.astype(np.int32),
+                step_w=step_w.astype(np.int32), step_k=step_k.astype(np.int32),
+                rhs_off=roff[:-1].astype(np.int64), rhs_bytes=rbytes.astype(np.int32),
+                stream=stream, rhs_len=int(roff[-1]), chunk_rows=R)
+    return host, rhs_slot
+
+
+class WaveDev:
+    def __init__(self, host):
+        self.host = host
+        self.t = {k: D.upload(host[k]) for k in ("chunk_step", "step_off", "step_bytes", "step_w",
+                                                 "step_k", "rhs_off", "rhs_bytes", "stream")}
+        self.desc = N.Wave(host["nchunks"], host["nsteps"], host["stage_max"], host["rhs_max"],
+                           *[D.ptr(self.t[k]) for k in ("chunk_step", "step_off", "step_bytes",
+                                                         "step_w", "step_k", "rhs_off",
+                                                         "rhs_bytes", "stream")])
+
+
 class DeviceBilu:
     """Level-ordered SELL-32 copies of the strict L and U factors."""
 
-    def __init__(self, F: BiluFactors):
+    def __init__(self, F: BiluFactors, use_wave: bool = True):
         D.require_cuda()
         b = F.block_size
         if b not in (1, 3):
@@ -165,10 +276,23 @@ class DeviceBilu:
         self.U = D.SellDev(hu)
         self.uinv = D.upload(ui)
         t = D.torch()
-        self.tickets = t.zeros(4, dtype=t.int32, device="cuda")
+        self.tickets = t.zeros(8, dtype=t.int32, device="cuda")
         self.work = D.empty(max(F.n * b, 1))
-        self.desc = N.Bilu(F.n, b, self.L.desc, self.U.desc, D.ptr(self.uinv), D.ptr(self.tickets))
         self.n, self.b = F.n, b
+        self.use_wave = bool(F.n > 0 and use_wave)
+        if self.use_wave:
+            hu, uslot = wave_plan(F.U, F.u_schedule, b, True, uinv=F.u_diag_inv)
+            hl, lslot = wave_plan(F.L, F.l_schedule, b, False, aux_slot=uslot)
+            self.Lw, self.Uw = WaveDev(hl), WaveDev(hu)
+            self.l_slot = D.upload(lslot.astype(np.int32))
+            self.rhs_l = D.zeros(max(hl["rhs_len"], 1))
+            self.rhs_u = D.zeros(max(hu["rhs_len"], 1))
+            wl, wu, ls, rl, ru = (self.Lw.desc, self.Uw.desc, D.ptr(self.l_slot),
+                                  D.ptr(self.rhs_l), D.ptr(self.rhs_u))
+        else:
+            wl, wu, ls, rl, ru = N.Wave(), N.Wave(), 0, 0, 0
+        self.desc = N.Bilu(F.n, b, self.L.desc, self.U.desc, D.ptr(self.uinv), D.ptr(self.tickets),
+                           1 if self.use_wave else 0, wl, wu, ls, rl, ru)
 
     def apply(self, r, z):
         N.check(N.lib().cprb_bilu_apply(C.byref(self.desc), D.ptr(r), D.ptr(z), D.ptr(self.work),
