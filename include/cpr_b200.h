@@ -225,6 +225,7 @@ int cprb_cpr_apply(const cprb_cpr* P, const double* r, double* z, void* stream);
 int cprb_graph_cache_create(void** out);
 int cprb_graph_cache_destroy(void* cache);
 int cprb_cpr_apply_graph(void* cache, const cprb_cpr* P, const double* r, double* z, void* stream);
+int cprb_amg_cycle_graph(void* cache, const cprb_amg* h, const double* r, double* z, void* stream);
 /* src/cpr.py:184-186  second half given zp already in P->zp. */
 int cprb_cpr_finish(const cprb_cpr* P, const double* r, double* z, void* stream);
 

@@ -88,6 +88,7 @@ _SIGS = {
     "cprb_graph_cache_create": (C.c_int, [C.POINTER(C.c_void_p)]),
     "cprb_graph_cache_destroy": (C.c_int, [vp]),
     "cprb_cpr_apply_graph": (C.c_int, [vp, C.POINTER(Cpr), vp, vp, vp]),
+    "cprb_amg_cycle_graph": (C.c_int, [vp, C.POINTER(Amg), vp, vp, vp]),
     "cprb_cpr_finish": (C.c_int, [C.POINTER(Cpr), vp, vp, vp]),
     "cprb_div_host": (C.c_int, [C.c_int64, vp, C.c_double, vp, vp]),
     "cprb_dot": (C.c_int, [C.c_int64, vp, vp, vp, vp, vp, vp]),

@@ -23,33 +23,37 @@ namespace cprb {
 // SCATTER: final value also written to out[perm[i]] (natural order).
 template <int ZG, int GATHER, int SCATTER>
 __global__ void __launch_bounds__(256)
-    k_sweep(const cprb_sell S, int s0, int s1, const double* __restrict__ diag, double* b,
-            const double* __restrict__ gsrc, int gstride, const int32_t* __restrict__ perm,
-            const double* xin, double* xout, double* __restrict__ sout) {
+    k_sweep(const cprb_sell S, int s0, int s1, int r0, int r1, const double* __restrict__ diag,
+            double* b, const double* __restrict__ gsrc, int gstride,
+            const int32_t* __restrict__ perm, const double* xin, double* xout,
+            double* __restrict__ sout) {
   const int w = s0 + (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (w >= s1) return;
+  // colours are contiguous row ranges padded to whole slices: the row is
+  // implied by the lane, so every per-row load below is independent
+  const int row = r0 + (w - s0) * 32 + lane;
+  if (row >= r1) return;
   const int lid = w * 32 + lane;
-  const int row = S.lane_row[lid];
-  if (row < 0) return;
-  const int len = ZG ? S.lane_len_lo[lid] : S.lane_len[lid];
-  const int64_t base = S.slice_ptr[w] + lane;
-  double acc = 0.0;
-#pragma unroll 4
-  for (int m = 0; m < len; ++m) {
-    const int64_t e = base + (int64_t)m * 32;
-    acc = acc + __ldg(S.vals + e) * __ldg(xin + __ldg(S.cols + e));
-  }
+  const int len = ZG ? __ldg(S.lane_len_lo + lid) : __ldg(S.lane_len + lid);
+  const int64_t base = __ldg(S.slice_ptr + w) + lane;
+  const double d = __ldg(diag + row);
   double bi;
   if (GATHER) {
-    bi = __ldg(gsrc + (int64_t)gstride * perm[row]);
+    bi = __ldg(gsrc + (int64_t)gstride * __ldg(perm + row));
     b[row] = bi;
   } else {
     bi = b[row];
   }
-  const double xn = (bi - acc) / diag[row];
+  double acc = 0.0;
+#pragma unroll 8
+  for (int m = 0; m < len; ++m) {
+    const int64_t e = base + (int64_t)m * 32;
+    acc = acc + __ldg(S.vals + e) * __ldg(xin + __ldg(S.cols + e));
+  }
+  const double xn = (bi - acc) / d;
   xout[row] = xn;
-  if (SCATTER) sout[perm[row]] = xn;
+  if (SCATTER) sout[__ldg(perm + row)] = xn;
 }
 
 __global__ void k_copy_rows(const cprb_sell S, int s0, int s1, const double* src, double* dst) {
@@ -142,12 +146,15 @@ __global__ void k_scatter(int n, const int32_t* __restrict__ idx, const double* 
 static inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
 template <int ZG, int G, int SC>
-static void launch_sweep(const cprb_amg_level& L, int s0, int s1, double* b, const double* gsrc,
+static void launch_sweep(const cprb_amg_level& L, int k, double* b, const double* gsrc,
                          int gstride, const int32_t* perm, const double* xin, double* xout,
                          double* sout, cudaStream_t st) {
+  const int s0 = L.color_slices[k], s1 = L.color_slices[k + 1];
   if (s1 <= s0) return;
-  k_sweep<ZG, G, SC><<<nblk((int64_t)(s1 - s0) * 32, 256), 256, 0, st>>>(
-      L.smoother, s0, s1, L.diag, b, gsrc, gstride, perm, xin, xout, sout);
+  const int threads = (s1 - s0) * 32 >= 256 ? 256 : 128;
+  k_sweep<ZG, G, SC><<<nblk((int64_t)(s1 - s0) * 32, threads), threads, 0, st>>>(
+      L.smoother, s0, s1, L.color_rows[k], L.color_rows[k + 1], L.diag, b, gsrc, gstride, perm,
+      xin, xout, sout);
 }
 
 int pgs_pass(const cprb_amg_level& L, const double* b_in, double* x, int dir, int zero_guess,
@@ -170,14 +177,14 @@ int pgs_pass(const cprb_amg_level& L, const double* b_in, double* x, int dir, in
     const int zg = zero_guess ? 1 : 0, g = gsrc ? 1 : 0, sc = sout ? 1 : 0;
     const int code = zg * 4 + g * 2 + sc;
     switch (code) {
-      case 0: launch_sweep<0, 0, 0>(L, s0, s1, b, gsrc, gstride, perm, x, xout, sout, st); break;
-      case 1: launch_sweep<0, 0, 1>(L, s0, s1, b, gsrc, gstride, perm, x, xout, sout, st); break;
-      case 2: launch_sweep<0, 1, 0>(L, s0, s1, b, gsrc, gstride, perm, x, xout, sout, st); break;
-      case 3: launch_sweep<0, 1, 1>(L, s0, s1, b, gsrc, gstride, perm, x, xout, sout, st); break;
-      case 4: launch_sweep<1, 0, 0>(L, s0, s1, b, gsrc, gstride, perm, x, xout, sout, st); break;
-      case 5: launch_sweep<1, 0, 1>(L, s0, s1, b, gsrc, gstride, perm, x, xout, sout, st); break;
-      case 6: launch_sweep<1, 1, 0>(L, s0, s1, b, gsrc, gstride, perm, x, xout, sout, st); break;
-      default: launch_sweep<1, 1, 1>(L, s0, s1, b, gsrc, gstride, perm, x, xout, sout, st); break;
+      case 0: launch_sweep<0, 0, 0>(L, k, b, gsrc, gstride, perm, x, xout, sout, st); break;
+      case 1: launch_sweep<0, 0, 1>(L, k, b, gsrc, gstride, perm, x, xout, sout, st); break;
+      case 2: launch_sweep<0, 1, 0>(L, k, b, gsrc, gstride, perm, x, xout, sout, st); break;
+      case 3: launch_sweep<0, 1, 1>(L, k, b, gsrc, gstride, perm, x, xout, sout, st); break;
+      case 4: launch_sweep<1, 0, 0>(L, k, b, gsrc, gstride, perm, x, xout, sout, st); break;
+      case 5: launch_sweep<1, 0, 1>(L, k, b, gsrc, gstride, perm, x, xout, sout, st); break;
+      case 6: launch_sweep<1, 1, 0>(L, k, b, gsrc, gstride, perm, x, xout, sout, st); break;
+      default: launch_sweep<1, 1, 1>(L, k, b, gsrc, gstride, perm, x, xout, sout, st); break;
     }
     if (snap && s1 > s0)
       k_copy_rows<<<nblk((int64_t)(s1 - s0) * 32, 256), 256, 0, st>>>(L.smoother, s0, s1, L.tmp, x);

@@ -45,16 +45,29 @@ int cprb_graph_cache_destroy(void* h) {
   return CPRB_OK;
 }
 
+int cprb_amg_cycle(const cprb_amg* h, const double* r, double* z, void* stream);
+
+static int graph_run(void* h, int op, const void* P, const double* r, double* z, void* stream);
+
 int cprb_cpr_apply_graph(void* h, const cprb_cpr* P, const double* r, double* z, void* stream) {
+  return graph_run(h, 0, P, r, z, stream);
+}
+
+int cprb_amg_cycle_graph(void* h, const cprb_amg* A, const double* r, double* z, void* stream) {
+  return graph_run(h, 1, A, r, z, stream);
+}
+
+static int graph_run(void* h, int op, const void* P, const double* r, double* z, void* stream) {
   auto* c = static_cast<GraphCache*>(h);
-  GraphCache::Key key{P, r, z};
+  GraphCache::Key key{(const char*)P + op, r, z};
   auto it = c->map.find(key);
   cudaGraphExec_t exec = nullptr;
   if (it == c->map.end()) {
     cudaGraph_t g = nullptr;
     if (cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
       return check_launch("begin capture");
-    int rc = cprb_cpr_apply(P, r, z, c->cap);
+    int rc = op == 0 ? cprb_cpr_apply((const cprb_cpr*)P, r, z, c->cap)
+                     : cprb_amg_cycle((const cprb_amg*)P, r, z, c->cap);
     cudaError_t e = cudaStreamEndCapture(c->cap, &g);
     if (rc) return rc;
     if (e != cudaSuccess) return set_error(CPRB_EDEVICE, std::string("end capture: ") + cudaGetErrorString(e));

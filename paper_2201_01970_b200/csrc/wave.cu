@@ -21,9 +21,10 @@
 
 namespace cprb {
 
-constexpr int WAVE_THREADS = 64;  // == wmax of the plan
-constexpr int WAVE_DEPTH = 6;
+constexpr int WAVE_THREADS = 128;  // == wmax of the plan
+constexpr int WAVE_DEPTH = 4;
 constexpr int WAVE_RING = 4;
+constexpr int WAVE_KPRE = 3;       // external dependencies prefetched per row
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -64,23 +65,74 @@ struct WaveSmem {
   int* chunk;         // 1
 };
 
-template <int B, int K, bool UPPER>
-__device__ __forceinline__ void wave_rowsum_fixed(const int32_t* codes, const double* vals, int Wp,
-                                                  int t, const double* ring, const double* glob,
-                                                  double* tsum) {
-  double v[K][B];
+template <int B>
+struct Pre {
+  double v[WAVE_KPRE][B];
+};
+
+__device__ __forceinline__ bool is_sentinel(double v) {
+  return (unsigned long long)__double_as_longlong(v) == CPRB_SENTINEL;
+}
+
+// issue (do not wait for) the loads of a row's cross-chunk dependencies
+template <int B>
+__device__ __forceinline__ void wave_prefetch(const int32_t* codes, int Wp, int t, int len,
+                                              const double* glob, Pre<B>& p) {
 #pragma unroll
-  for (int m = 0; m < K; ++m) {
-    const int code = codes[m * Wp + t];
-    if (code < 0) {
-      const double* s = ring + (int64_t)(-code - 1) * B;
+  for (int m = 0; m < WAVE_KPRE; ++m) {
+    if (m < len) {
+      const int code = codes[m * Wp + t];
+      if (code >= 0) {
 #pragma unroll
-      for (int c = 0; c < B; ++c) v[m][c] = s[c];
-    } else {
-#pragma unroll
-      for (int c = 0; c < B; ++c) v[m][c] = wait_value(glob + (int64_t)B * code + c);
+        for (int c = 0; c < B; ++c) p.v[m][c] = ld_relaxed(glob + (int64_t)B * code + c);
+      }
     }
   }
+}
+
+// all B components polled concurrently until none is the sentinel
+template <int B>
+__device__ __forceinline__ void wait_block(const double* g, double* v) {
+  int spins = 0;
+  while (true) {
+    bool ok = true;
+#pragma unroll
+    for (int c = 0; c < B; ++c) ok &= !is_sentinel(v[c]);
+    if (ok) return;
+    if (++spins > 8) __nanosleep(20);
+#pragma unroll
+    for (int c = 0; c < B; ++c)
+      if (is_sentinel(v[c])) v[c] = ld_relaxed(g + c);
+  }
+}
+
+template <int B>
+__device__ __forceinline__ void dep_value(int code, int m, const double* ring, const double* glob,
+                                          const Pre<B>& p, double* v) {
+  if (code < 0) {
+    const double* s = ring + (int64_t)(-code - 1) * B;
+#pragma unroll
+    for (int c = 0; c < B; ++c) v[c] = s[c];
+    return;
+  }
+  const double* g = glob + (int64_t)B * code;
+  if (m < WAVE_KPRE) {
+#pragma unroll
+    for (int c = 0; c < B; ++c) v[c] = p.v[m][c];
+  } else {
+#pragma unroll
+    for (int c = 0; c < B; ++c) v[c] = ld_relaxed(g + c);
+  }
+  wait_block<B>(g, v);
+}
+
+template <int B, int K>
+__device__ __forceinline__ void wave_rowsum_fixed(const int32_t* codes, const double* vals, int Wp,
+                                                  int t, const double* ring, const double* glob,
+                                                  const Pre<B>& pre, double* tsum) {
+  double v[K][B];
+#pragma unroll
+  for (int m = 0; m < K; ++m) dep_value<B>(codes[m * Wp + t], m, ring, glob, pre, v[m]);
 #pragma unroll
   for (int r = 0; r < B; ++r) {
     double p[K];
@@ -98,17 +150,15 @@ __device__ __forceinline__ void wave_rowsum_fixed(const int32_t* codes, const do
 template <int B>
 __device__ __forceinline__ void wave_rowsum_generic(const int32_t* codes, const double* vals,
                                                     int Wp, int t, int len, const double* ring,
-                                                    const double* glob, double* tsum) {
+                                                    const double* glob, const Pre<B>& pre,
+                                                    double* tsum) {
 #pragma unroll
   for (int r = 0; r < B; ++r) {
     auto f = [&](int m) -> double {
-      const int code = codes[m * Wp + t];
       double v[B], mr[B];
+      dep_value<B>(codes[m * Wp + t], m, ring, glob, pre, v);
 #pragma unroll
-      for (int c = 0; c < B; ++c) {
-        v[c] = code < 0 ? ring[(int64_t)(-code - 1) * B + c] : wait_value(glob + (int64_t)B * code + c);
-        mr[c] = vals[(int64_t)(m * B * B + r * B + c) * Wp + t];
-      }
+      for (int c = 0; c < B; ++c) mr[c] = vals[(int64_t)(m * B * B + r * B + c) * Wp + t];
       return block_row_dot<B>(mr, v);
     };
     tsum[r] = segsum_rt(f, len);
@@ -162,6 +212,16 @@ __global__ void __launch_bounds__(WAVE_THREADS, 1)
     const int s0 = W.chunk_step[c], s1 = W.chunk_step[c + 1];
     if (tid == 0)
       for (int k = s0; k < s1 && k < s0 + WAVE_DEPTH; ++k) issue(k, g + (k - s0));
+    Pre<B> pre;
+    // prefetch the first step's cross-chunk dependencies
+    {
+      const int st = g % WAVE_DEPTH;
+      mbar_wait(&S.bar[st], (g / WAVE_DEPTH) & 1);
+      const int w = W.step_w[s0];
+      const int Wp = (w + 3) & ~3;
+      const int32_t* rows = reinterpret_cast<const int32_t*>(S.stage + (size_t)st * stage_max);
+      if (tid < w) wave_prefetch<B>(rows + 3 * Wp, Wp, tid, rows[Wp + tid], out_nat, pre);
+    }
     for (int k = s0; k < s1; ++k, ++g) {
       const int st = g % WAVE_DEPTH;
       mbar_wait(&S.bar[st], (g / WAVE_DEPTH) & 1);
@@ -172,6 +232,17 @@ __global__ void __launch_bounds__(WAVE_THREADS, 1)
       const int32_t* lens = rows + Wp;
       const int32_t* aux = lens + Wp;
       const int32_t* codes = aux + Wp;
+      // issue the next step's cross-chunk dependency loads now, so their L2
+      // round trip overlaps this step
+      Pre<B> nxt;
+      if (k + 1 < s1) {
+        const int st1 = (g + 1) % WAVE_DEPTH;
+        mbar_wait(&S.bar[st1], ((g + 1) / WAVE_DEPTH) & 1);
+        const int w1 = W.step_w[k + 1];
+        const int Wp1 = (w1 + 3) & ~3;
+        const int32_t* r1 = reinterpret_cast<const int32_t*>(S.stage + (size_t)st1 * stage_max);
+        if (tid < w1) wave_prefetch<B>(r1 + 3 * Wp1, Wp1, tid, r1[Wp1 + tid], out_nat, nxt);
+      }
       const double* vals = reinterpret_cast<const double*>(blk + (size_t)(12 + 4 * K) * Wp);
       const double* uinv = vals + (size_t)K * BB * Wp;
       const double* rhs = S.rhs + (size_t)st * (rhs_max / 8);
@@ -186,10 +257,10 @@ __global__ void __launch_bounds__(WAVE_THREADS, 1)
 #pragma unroll
             for (int r = 0; r < B; ++r) ts[r] = 0.0;
             break;
-          case 1: wave_rowsum_fixed<B, 1, UPPER>(codes, vals, Wp, tid, S.ring, out_nat, ts); break;
-          case 2: wave_rowsum_fixed<B, 2, UPPER>(codes, vals, Wp, tid, S.ring, out_nat, ts); break;
-          case 3: wave_rowsum_fixed<B, 3, UPPER>(codes, vals, Wp, tid, S.ring, out_nat, ts); break;
-          default: wave_rowsum_generic<B>(codes, vals, Wp, tid, len, S.ring, out_nat, ts); break;
+          case 1: wave_rowsum_fixed<B, 1>(codes, vals, Wp, tid, S.ring, out_nat, pre, ts); break;
+          case 2: wave_rowsum_fixed<B, 2>(codes, vals, Wp, tid, S.ring, out_nat, pre, ts); break;
+          case 3: wave_rowsum_fixed<B, 3>(codes, vals, Wp, tid, S.ring, out_nat, pre, ts); break;
+          default: wave_rowsum_generic<B>(codes, vals, Wp, tid, len, S.ring, out_nat, pre, ts); break;
         }
         double res[B];
         if constexpr (!UPPER) {
@@ -227,6 +298,7 @@ __global__ void __launch_bounds__(WAVE_THREADS, 1)
       }
       __syncthreads();  // ring + stage buffer reuse
       if (tid == 0 && k + WAVE_DEPTH < s1) issue(k + WAVE_DEPTH, g + WAVE_DEPTH);
+      pre = nxt;
     }
   }
 }

@@ -151,9 +151,10 @@ def _level_sell(T: BlockCsrMatrix, sched: LevelSchedule, b: int, uinv=None):
     return h, ui
 
 
-WAVE_WMAX = 64          # rows per step == threads per CTA (csrc/wave.cu)
+WAVE_WMAX = 128         # rows per step == threads per CTA (csrc/wave.cu)
 WAVE_RING = 4           # steps kept in the shared-memory ring
-WAVE_STAGE_CAP = 24576  # bytes per streamed step
+WAVE_STAGE_CAP = 40960  # bytes per streamed step
+WAVE_BANDS = 2          # dependency bandwidths (xy-planes) per chunk
 
 
 def _round16(x):
@@ -174,7 +175,7 @@ def wave_plan(T: BlockCsrMatrix, sched: LevelSchedule, b: int, upper: bool, uinv
     for li, lv in enumerate(sched.levels):
         level[lv] = li
     bw = int(np.abs(rows_of - cols).max()) if cols.size else 1
-    R = max(bw, -(-n // nchunk_min), 1)
+    R = max(WAVE_BANDS * bw, -(-n // nchunk_min), 1)
     pos = (n - 1 - np.arange(n)) if upper else np.arange(n)
     chunk = pos // R
     order = np.lexsort((np.arange(n), level, chunk))     # rows by (chunk, level, index)
