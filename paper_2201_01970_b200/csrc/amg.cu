@@ -21,39 +21,60 @@ namespace cprb {
 // GATHER: b_i = src[stride * perm[i]] (level-0 CPR restriction, src/cpr.py:132)
 //         and it is stored into b for the rest of the cycle.
 // SCATTER: final value also written to out[perm[i]] (natural order).
+constexpr int SWEEP_PRE = 8;  // entries held in registers across the PDL wait
+
 template <int ZG, int GATHER, int SCATTER>
 __global__ void __launch_bounds__(256)
     k_sweep(const cprb_sell S, int s0, int s1, int r0, int r1, const double* __restrict__ diag,
             double* b, const double* __restrict__ gsrc, int gstride,
             const int32_t* __restrict__ perm, const double* xin, double* xout,
             double* __restrict__ sout) {
+  pdl_trigger();
   const int w = s0 + (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
-  if (w >= s1) return;
   // colours are contiguous row ranges padded to whole slices: the row is
-  // implied by the lane, so every per-row load below is independent
+  // implied by the lane.  Everything before pdl_wait() is static matrix data.
   const int row = r0 + (w - s0) * 32 + lane;
-  if (row >= r1) return;
-  const int lid = w * 32 + lane;
-  const int len = ZG ? __ldg(S.lane_len_lo + lid) : __ldg(S.lane_len + lid);
-  const int64_t base = __ldg(S.slice_ptr + w) + lane;
-  const double d = __ldg(diag + row);
+  const bool active = (w < s1) && (row < r1);
+  int len = 0;
+  int64_t base = 0;
+  double d = 1.0;
+  int colr[SWEEP_PRE];
+  double valr[SWEEP_PRE];
+  int pidx = 0;
+  if (active) {
+    const int lid = w * 32 + lane;
+    len = ZG ? __ldg(S.lane_len_lo + lid) : __ldg(S.lane_len + lid);
+    base = __ldg(S.slice_ptr + w) + lane;
+    d = __ldg(diag + row);
+    if (GATHER || SCATTER) pidx = __ldg(perm + row);
+#pragma unroll
+    for (int m = 0; m < SWEEP_PRE; ++m)
+      if (m < len) {
+        colr[m] = __ldg(S.cols + base + (int64_t)m * 32);
+        valr[m] = __ldg(S.vals + base + (int64_t)m * 32);
+      }
+  }
+  pdl_wait();
+  if (!active) return;
   double bi;
   if (GATHER) {
-    bi = __ldg(gsrc + (int64_t)gstride * __ldg(perm + row));
+    bi = gsrc[(int64_t)gstride * pidx];
     b[row] = bi;
   } else {
     bi = b[row];
   }
   double acc = 0.0;
-#pragma unroll 8
-  for (int m = 0; m < len; ++m) {
+#pragma unroll
+  for (int m = 0; m < SWEEP_PRE; ++m)
+    if (m < len) acc = acc + valr[m] * xin[colr[m]];
+  for (int m = SWEEP_PRE; m < len; ++m) {
     const int64_t e = base + (int64_t)m * 32;
-    acc = acc + __ldg(S.vals + e) * __ldg(xin + __ldg(S.cols + e));
+    acc = acc + __ldg(S.vals + e) * xin[__ldg(S.cols + e)];
   }
   const double xn = (bi - acc) / d;
   xout[row] = xn;
-  if (SCATTER) sout[__ldg(perm + row)] = xn;
+  if (SCATTER) sout[pidx] = xn;
 }
 
 __global__ void k_copy_rows(const cprb_sell S, int s0, int s1, const double* src, double* dst) {
@@ -85,47 +106,111 @@ __global__ void k_gs_sequential(const cprb_sell S, int n, const double* diag, co
 
 // residual r_i = b_i - A_l x (row in original column order, reduceat sum)
 // fused with restriction rc[I] = (0 + r_{i1}) + r_{i2}  (np.bincount order).
+constexpr int RR_PRE = 16;
+
+template <int K>
+__device__ __forceinline__ double rr_sum_fixed(const int* colr, const double* valr,
+                                               const double* x) {
+  double e[K];
+#pragma unroll
+  for (int m = 0; m < K; ++m) e[m] = valr[m] * x[colr[m]];
+  return segsum_fixed<K>(e);
+}
+
 __global__ void __launch_bounds__(256)
     k_resid_restrict(const cprb_sell R, const double* __restrict__ b,
                      const double* __restrict__ x, double* __restrict__ bc) {
+  pdl_trigger();
   const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
-  if (w >= R.nslices) return;  // warp-uniform
+  const bool wok = w < R.nslices;  // warp-uniform
   const int lid = w * 32 + lane;
-  const int row = R.lane_row[lid];
+  int row = -1, len = 0, out = -1;
+  int64_t base = 0;
+  int colr[RR_PRE];
+  double valr[RR_PRE];
+  if (wok) {
+    row = __ldg(R.lane_row + lid);
+    len = __ldg(R.lane_len + lid);
+    base = __ldg(R.slice_ptr + w) + lane;
+    if ((lane & 1) == 0) out = __ldg(R.agg_out + w * 16 + (lane >> 1));
+#pragma unroll
+    for (int m = 0; m < RR_PRE; ++m)
+      if (m < len) {
+        colr[m] = __ldg(R.cols + base + (int64_t)m * 32);
+        valr[m] = __ldg(R.vals + base + (int64_t)m * 32);
+      }
+  }
+  pdl_wait();
+  if (!wok) return;
   double res = 0.0;
   if (row >= 0) {
-    const int len = R.lane_len[lid];
-    const int64_t base = R.slice_ptr[w] + lane;
-    auto f = [&](int m) -> double {
-      const int64_t e = base + (int64_t)m * 32;
-      return __ldg(R.vals + e) * __ldg(x + __ldg(R.cols + e));
-    };
-    res = b[row] - segsum_rt(f, len);
+    double t;
+    switch (len) {
+      case 0: t = 0.0; break;
+      case 1: t = rr_sum_fixed<1>(colr, valr, x); break;
+      case 2: t = rr_sum_fixed<2>(colr, valr, x); break;
+      case 3: t = rr_sum_fixed<3>(colr, valr, x); break;
+      case 4: t = rr_sum_fixed<4>(colr, valr, x); break;
+      case 5: t = rr_sum_fixed<5>(colr, valr, x); break;
+      case 6: t = rr_sum_fixed<6>(colr, valr, x); break;
+      case 7: t = rr_sum_fixed<7>(colr, valr, x); break;
+      case 8: t = rr_sum_fixed<8>(colr, valr, x); break;
+      case 9: t = rr_sum_fixed<9>(colr, valr, x); break;
+      case 10: t = rr_sum_fixed<10>(colr, valr, x); break;
+      case 11: t = rr_sum_fixed<11>(colr, valr, x); break;
+      case 12: t = rr_sum_fixed<12>(colr, valr, x); break;
+      case 13: t = rr_sum_fixed<13>(colr, valr, x); break;
+      case 14: t = rr_sum_fixed<14>(colr, valr, x); break;
+      case 15: t = rr_sum_fixed<15>(colr, valr, x); break;
+      case 16: t = rr_sum_fixed<16>(colr, valr, x); break;
+      default: {
+        auto f = [&](int m) -> double {
+          const int64_t e = base + (int64_t)m * 32;
+          return __ldg(R.vals + e) * x[__ldg(R.cols + e)];
+        };
+        t = segsum_rt(f, len);
+      }
+    }
+    res = b[row] - t;
   }
   const double other = __shfl_down_sync(CPRB_FULL, res, 1);
-  if ((lane & 1) == 0) {
-    const int out = R.agg_out[w * 16 + (lane >> 1)];
-    if (out >= 0) bc[out] = (0.0 + res) + other;
-  }
+  if ((lane & 1) == 0 && out >= 0) bc[out] = (0.0 + res) + other;
 }
 
 // prolongation-correct x += ec[agg]  (src/amg.py:264)
 __global__ void k_prolong(int n, const int32_t* __restrict__ aggp, const double* __restrict__ xc,
                           double* __restrict__ x) {
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) x[i] = x[i] + xc[aggp[i]];
+  const int a = i < n ? __ldg(aggp + i) : 0;
+  pdl_wait();
+  if (i < n) x[i] = x[i] + xc[a];
 }
 
 // coarsest solve: x = inv(A_L) b, one warp per row, fixed lane/shuffle order
 __global__ void k_dense_mv(int n, const double* __restrict__ inv, const double* __restrict__ b,
                            double* __restrict__ x, const int32_t* __restrict__ out_idx) {
+  pdl_trigger();
   const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
+  constexpr int PRE = 8;
+  double a[PRE];
+  const double* row = inv + (int64_t)(w < n ? w : 0) * n;
+#pragma unroll
+  for (int k = 0; k < PRE; ++k) {
+    const int c = lane + 32 * k;
+    a[k] = (w < n && c < n) ? __ldg(row + c) : 0.0;
+  }
+  pdl_wait();
   if (w >= n) return;
-  const double* row = inv + (int64_t)w * n;
   double s = 0.0;
-  for (int c = lane; c < n; c += 32) s = s + row[c] * b[c];
+#pragma unroll
+  for (int k = 0; k < PRE; ++k) {
+    const int c = lane + 32 * k;
+    if (c < n) s = s + a[k] * b[c];
+  }
+  for (int c = lane + 32 * PRE; c < n; c += 32) s = s + row[c] * b[c];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s = s + __shfl_xor_sync(CPRB_FULL, s, o);
   if (lane == 0) x[out_idx ? out_idx[w] : w] = s;
@@ -152,9 +237,9 @@ static void launch_sweep(const cprb_amg_level& L, int k, double* b, const double
   const int s0 = L.color_slices[k], s1 = L.color_slices[k + 1];
   if (s1 <= s0) return;
   const int threads = (s1 - s0) * 32 >= 256 ? 256 : 128;
-  k_sweep<ZG, G, SC><<<nblk((int64_t)(s1 - s0) * 32, threads), threads, 0, st>>>(
-      L.smoother, s0, s1, L.color_rows[k], L.color_rows[k + 1], L.diag, b, gsrc, gstride, perm,
-      xin, xout, sout);
+  launch_pdl(k_sweep<ZG, G, SC>, nblk((int64_t)(s1 - s0) * 32, threads), threads, 0, st,
+             L.smoother, s0, s1, L.color_rows[k], L.color_rows[k + 1], L.diag, b, gsrc, gstride,
+             perm, xin, xout, sout);
 }
 
 int pgs_pass(const cprb_amg_level& L, const double* b_in, double* x, int dir, int zero_guess,
@@ -206,15 +291,15 @@ int amg_vcycle(const cprb_amg& h, const double* r, double* z, cudaStream_t st) {
     if (rc) return rc;
     double* bc = (l + 1 < nl - 1) ? h.levels[l + 1].b : h.coarse_b;
     if (L.restrict_op.nslices > 0)
-      k_resid_restrict<<<nblk((int64_t)L.restrict_op.nslices * 32, 256), 256, 0, st>>>(
-          L.restrict_op, L.b, L.x, bc);
+      launch_pdl(k_resid_restrict, nblk((int64_t)L.restrict_op.nslices * 32, 256), 256, 0, st,
+                 L.restrict_op, (const double*)L.b, (const double*)L.x, bc);
   }
-  k_dense_mv<<<nblk((int64_t)h.n_coarse * 32, 256), 256, 0, st>>>(h.n_coarse, h.coarse_inv,
-                                                                   h.coarse_b, h.coarse_x, nullptr);
+  launch_pdl(k_dense_mv, nblk((int64_t)h.n_coarse * 32, 256), 256, 0, st, h.n_coarse,
+             h.coarse_inv, (const double*)h.coarse_b, h.coarse_x, (const int32_t*)nullptr);
   for (int l = nl - 2; l >= 0; --l) {
     const cprb_amg_level& L = h.levels[l];
     const double* xc = (l + 1 < nl - 1) ? h.levels[l + 1].x : h.coarse_x;
-    k_prolong<<<nblk(L.n, 256), 256, 0, st>>>(L.n, L.aggp, xc, L.x);
+    launch_pdl(k_prolong, nblk(L.n, 256), 256, 0, st, L.n, L.aggp, xc, L.x);
     int rc = pgs_pass(L, L.b, L.x, 1, 0, nullptr, 0, h.perm0, l == 0 ? z : nullptr, st);
     if (rc) return rc;
   }

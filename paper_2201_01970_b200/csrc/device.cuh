@@ -138,6 +138,11 @@ __device__ __forceinline__ double block_row_dot(const double* m, const double* v
   }
 }
 
+// Programmatic Dependent Launch: let the next grid start its prologue now;
+// wait until every prerequisite grid finished (and its writes are visible).
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ void flag_nonfinite(int32_t* flag, bool bad) {
   if (flag && bad) atomicOr(flag, 1);
 }

@@ -6,7 +6,28 @@
 
 #include "../../include/cpr_b200.h"
 
+#include <utility>
+
 namespace cprb {
+
+// launch with programmatic stream serialization (PDL); kernels call
+// pdl_trigger() early and pdl_wait() before touching data of earlier grids
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 int set_error(int code, const std::string& msg);
 int check_launch(const char* what);
 

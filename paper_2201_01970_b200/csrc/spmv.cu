@@ -71,6 +71,8 @@ __global__ void __launch_bounds__(256) k_bsr(const cprb_sell A, const double* __
                                              double* __restrict__ out, int32_t* flag,
                                              double* __restrict__ sent,
                                              const int32_t* __restrict__ out_idx) {
+  pdl_trigger();
+  pdl_wait();
   const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (w >= A.nslices) return;
@@ -113,7 +115,7 @@ static void launch_bsr(const cprb_sell& A, const double* x, const double* rhs, d
   if (A.nslices <= 0) return;
   const int threads = 256;
   const int blocks = (A.nslices * 32 + threads - 1) / threads;
-  k_bsr<B, MODE><<<blocks, threads, 0, st>>>(A, x, rhs, out, flag, sent, oi);
+  launch_pdl(k_bsr<B, MODE>, blocks, threads, 0, st, A, x, rhs, out, flag, sent, oi);
 }
 
 int bsr_op(int mode, const cprb_sell& A, int b, const double* x, const double* rhs, double* out,

@@ -25,6 +25,16 @@ constexpr int WAVE_THREADS = 128;  // == wmax of the plan
 constexpr int WAVE_DEPTH = 4;
 constexpr int WAVE_RING = 4;
 constexpr int WAVE_KPRE = 3;       // external dependencies prefetched per row
+constexpr int WAVE_META = 1024;    // step metadata staged in shared memory per chunk
+
+struct StepMeta {
+  int64_t off;      // stream byte offset
+  int64_t rhs_off;  // rhs double offset
+  int32_t bytes;
+  int32_t rhs_bytes;
+  int32_t w;
+  int32_t k;
+};
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -61,6 +71,7 @@ struct WaveSmem {
   uint8_t* stage;     // DEPTH * stage_max
   double* rhs;        // DEPTH * rhs_max/8
   double* ring;       // RING * WAVE_THREADS * B
+  StepMeta* meta;     // WAVE_META
   uint64_t* bar;      // DEPTH
   int* chunk;         // 1
 };
@@ -181,7 +192,8 @@ __global__ void __launch_bounds__(WAVE_THREADS, 1)
   S.stage = smem_raw;
   S.rhs = reinterpret_cast<double*>(smem_raw + (size_t)WAVE_DEPTH * stage_max);
   S.ring = S.rhs + (size_t)WAVE_DEPTH * (rhs_max / 8);
-  S.bar = reinterpret_cast<uint64_t*>(S.ring + (size_t)WAVE_RING * WAVE_THREADS * B);
+  S.meta = reinterpret_cast<StepMeta*>(S.ring + (size_t)WAVE_RING * WAVE_THREADS * B);
+  S.bar = reinterpret_cast<uint64_t*>(S.meta + WAVE_META);
   S.chunk = reinterpret_cast<int*>(S.bar + WAVE_DEPTH);
   if (tid == 0) {
     for (int d = 0; d < WAVE_DEPTH; ++d) mbar_init(&S.bar[d], 1);
@@ -190,13 +202,26 @@ __global__ void __launch_bounds__(WAVE_THREADS, 1)
   __syncthreads();
   uint32_t g = 0;  // steps consumed by this CTA (stage = g % DEPTH, parity = (g / DEPTH) & 1)
 
+  int s0 = 0;
+  bool staged = false;
+  // step metadata: from shared memory when the chunk's steps were staged
+  auto meta = [&](int k) -> StepMeta {
+    if (staged) return S.meta[k - s0];
+    StepMeta m;
+    m.off = W.step_off[k];
+    m.rhs_off = W.rhs_off[k];
+    m.bytes = W.step_bytes[k];
+    m.rhs_bytes = W.rhs_bytes[k];
+    m.w = W.step_w[k];
+    m.k = W.step_k[k];
+    return m;
+  };
   auto issue = [&](int k, uint32_t gg) {
     const int st = gg % WAVE_DEPTH;
-    const uint32_t sb = W.step_bytes[k];
-    const uint32_t rb = W.rhs_bytes[k];
-    mbar_expect_tx(&S.bar[st], sb + rb);
-    bulk_g2s(S.stage + (size_t)st * stage_max, W.stream + W.step_off[k], sb, &S.bar[st]);
-    bulk_g2s(S.rhs + (size_t)st * (rhs_max / 8), rhs_steps + W.rhs_off[k], rb, &S.bar[st]);
+    const StepMeta m = meta(k);
+    mbar_expect_tx(&S.bar[st], (uint32_t)(m.bytes + m.rhs_bytes));
+    bulk_g2s(S.stage + (size_t)st * stage_max, W.stream + m.off, m.bytes, &S.bar[st]);
+    bulk_g2s(S.rhs + (size_t)st * (rhs_max / 8), rhs_steps + m.rhs_off, m.rhs_bytes, &S.bar[st]);
   };
 
   while (true) {
@@ -207,9 +232,24 @@ __global__ void __launch_bounds__(WAVE_THREADS, 1)
     }
     __syncthreads();
     const int c = *S.chunk;
-    __syncthreads();
+    __syncthreads();  // also: everyone is done with the previous chunk's metadata
     if (c >= W.nchunks) break;
-    const int s0 = W.chunk_step[c], s1 = W.chunk_step[c + 1];
+    s0 = W.chunk_step[c];
+    const int s1 = W.chunk_step[c + 1];
+    staged = (s1 - s0) <= WAVE_META;
+    if (staged) {
+      for (int k = s0 + tid; k < s1; k += blockDim.x) {
+        StepMeta m;
+        m.off = W.step_off[k];
+        m.rhs_off = W.rhs_off[k];
+        m.bytes = W.step_bytes[k];
+        m.rhs_bytes = W.rhs_bytes[k];
+        m.w = W.step_w[k];
+        m.k = W.step_k[k];
+        S.meta[k - s0] = m;
+      }
+      __syncthreads();
+    }
     if (tid == 0)
       for (int k = s0; k < s1 && k < s0 + WAVE_DEPTH; ++k) issue(k, g + (k - s0));
     Pre<B> pre;
@@ -217,7 +257,7 @@ __global__ void __launch_bounds__(WAVE_THREADS, 1)
     {
       const int st = g % WAVE_DEPTH;
       mbar_wait(&S.bar[st], (g / WAVE_DEPTH) & 1);
-      const int w = W.step_w[s0];
+      const int w = meta(s0).w;
       const int Wp = (w + 3) & ~3;
       const int32_t* rows = reinterpret_cast<const int32_t*>(S.stage + (size_t)st * stage_max);
       if (tid < w) wave_prefetch<B>(rows + 3 * Wp, Wp, tid, rows[Wp + tid], out_nat, pre);
@@ -226,7 +266,8 @@ __global__ void __launch_bounds__(WAVE_THREADS, 1)
       const int st = g % WAVE_DEPTH;
       mbar_wait(&S.bar[st], (g / WAVE_DEPTH) & 1);
       const uint8_t* blk = S.stage + (size_t)st * stage_max;
-      const int w = W.step_w[k], K = W.step_k[k];
+      const StepMeta mk = meta(k);
+      const int w = mk.w, K = mk.k;
       const int Wp = (w + 3) & ~3;
       const int32_t* rows = reinterpret_cast<const int32_t*>(blk);
       const int32_t* lens = rows + Wp;
@@ -238,7 +279,7 @@ __global__ void __launch_bounds__(WAVE_THREADS, 1)
       if (k + 1 < s1) {
         const int st1 = (g + 1) % WAVE_DEPTH;
         mbar_wait(&S.bar[st1], ((g + 1) / WAVE_DEPTH) & 1);
-        const int w1 = W.step_w[k + 1];
+        const int w1 = meta(k + 1).w;
         const int Wp1 = (w1 + 3) & ~3;
         const int32_t* r1 = reinterpret_cast<const int32_t*>(S.stage + (size_t)st1 * stage_max);
         if (tid < w1) wave_prefetch<B>(r1 + 3 * Wp1, Wp1, tid, r1[Wp1 + tid], out_nat, nxt);
@@ -313,7 +354,7 @@ __global__ void k_scatter_slots(int n, int b, const int32_t* __restrict__ slot,
 
 static size_t wave_smem(const cprb_wave& W, int b) {
   return (size_t)WAVE_DEPTH * (W.stage_max + W.rhs_max) + (size_t)WAVE_RING * WAVE_THREADS * b * 8 +
-         WAVE_DEPTH * 8 + 16;
+         sizeof(StepMeta) * WAVE_META + WAVE_DEPTH * 8 + 16;
 }
 
 template <int B, bool UPPER>
