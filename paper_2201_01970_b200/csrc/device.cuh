@@ -124,6 +124,47 @@ __device__ __forceinline__ double segsum_rt(const F& f, int L) {
   return a0 + pairwise_rec(f, 1, n);
 }
 
+// reduceat segment of runtime length L <= N held in registers e[0..N-1]
+// (entries >= L are ignored): e[0] + pairwise(e[1:L]) with predicated,
+// branch-free accumulation so that lanes of different length stay converged.
+// The n < 8 sequential part starts from -0.0, the exact additive identity.
+template <int N>
+__device__ __forceinline__ double segsum_masked(const double* e, int L) {
+  static_assert(N <= 129, "segsum_masked handles rows of at most 129 entries");
+  if constexpr (N == 0) {
+    return 0.0;
+  } else {
+    const int n = L - 1;  // entries in the pairwise part
+    double s = -0.0;
+    if constexpr (N - 1 < 8) {
+#pragma unroll
+      for (int t = 0; t < N - 1; ++t)
+        if (t < n) s = s + e[1 + t];
+    } else {
+      if (n < 8) {
+#pragma unroll
+        for (int t = 0; t < 7; ++t)
+          if (t < n) s = s + e[1 + t];
+      } else {
+        const int nf = n & ~7;
+        double r[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) r[k] = e[1 + k];
+#pragma unroll
+        for (int g = 8; g + 8 <= N - 1; g += 8)
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (g < nf) r[k] = r[k] + e[1 + g + k];
+        s = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+#pragma unroll
+        for (int t = 8; t < N - 1; ++t)
+          if (t >= nf && t < n) s = s + e[1 + t];
+      }
+    }
+    return L > 0 ? e[0] + s : 0.0;
+  }
+}
+
 // np.einsum('kij,kj->ki') row r of a b x b block times a b-vector
 // (b = 3: (p0 + p2) + p1; b = 1: p0)
 template <int B>

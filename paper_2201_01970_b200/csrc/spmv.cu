@@ -12,109 +12,102 @@ namespace cprb {
 // MODE 1: out = rhs - A x
 // MODE 2: out = rhs - A (Pi x)  with Pi scattering x (nb) into block slot 0
 //         (src/cpr.py:184-185); only the c = 0 value planes are read.
+//
+// Work split: B warps per SELL slice, warp r computes scalar output row r of
+// the slice's 32 block rows (so each thread holds one expanded row: 3K values,
+// K columns, 3K x entries -> ~60 registers, 4x the occupancy of a thread per
+// block row).  The slice width (max blocks per row) is warp-uniform; every
+// lane walks it with predication and sums with segsum_masked, so lanes with
+// shorter rows (grid boundaries) never split the warp.  Value planes (r, c)
+// of a slot are 256-byte coalesced warp loads; the x gathers of the B warps
+// of a slice hit the same L1 lines.
+constexpr int BSR_WARPS = 6;  // warps per CTA (2 slices of a 3x3 BSR)
+
 template <int B, int MODE, int K>
-__device__ __forceinline__ void bsr_row_fixed(const cprb_sell& A, int64_t base, int lane,
-                                              const double* __restrict__ x, double* res) {
+__device__ __forceinline__ double bsr_row_k(const cprb_sell& A, int64_t base, int lane, int r,
+                                            int len, const double* __restrict__ x) {
   int col[K];
 #pragma unroll
-  for (int m = 0; m < K; ++m) col[m] = __ldg(A.cols + base + (int64_t)m * 32 + lane);
-  double xv[B * K];
+  for (int m = 0; m < K; ++m) col[m] = (m < len) ? __ldg(A.cols + base + (int64_t)m * 32 + lane) : 0;
+  double e[B * K];
 #pragma unroll
-  for (int m = 0; m < K; ++m)
+  for (int m = 0; m < K; ++m) {
+    const double* vp = A.vals + (base + (int64_t)m * 32) * (B * B) + (int64_t)(r * B) * 32 + lane;
 #pragma unroll
     for (int c = 0; c < B; ++c) {
-      if constexpr (MODE == 2)
-        xv[B * m + c] = (c == 0) ? __ldg(x + col[m]) : 0.0;
-      else
-        xv[B * m + c] = __ldg(x + (int64_t)B * col[m] + c);
-    }
-#pragma unroll
-  for (int r = 0; r < B; ++r) {
-    double e[B * K];
-#pragma unroll
-    for (int m = 0; m < K; ++m)
-#pragma unroll
-      for (int c = 0; c < B; ++c) {
-        if (MODE == 2 && c != 0) {
-          e[B * m + c] = 0.0;
-        } else {
-          const double v = __ldg(A.vals + (base + (int64_t)m * 32) * (B * B) +
-                                 (int64_t)(r * B + c) * 32 + lane);
-          e[B * m + c] = v * xv[B * m + c];
-        }
+      if (MODE == 2 && c != 0) {
+        e[B * m + c] = 0.0;
+      } else if (m < len) {
+        const double xv = (MODE == 2) ? __ldg(x + col[m]) : __ldg(x + (int64_t)B * col[m] + c);
+        e[B * m + c] = __ldg(vp + c * 32) * xv;
+      } else {
+        e[B * m + c] = 0.0;
       }
-    res[r] = segsum_fixed<B * K>(e);
+    }
   }
+  return segsum_masked<B * K>(e, B * len);
 }
 
 template <int B, int MODE>
-__device__ __forceinline__ void bsr_row_generic(const cprb_sell& A, int64_t base, int lane,
-                                                int len, const double* __restrict__ x,
-                                                double* res) {
-#pragma unroll
-  for (int r = 0; r < B; ++r) {
-    auto f = [&](int t) -> double {
-      const int m = t / B, c = t - m * B;
-      if (MODE == 2 && c != 0) return 0.0;
-      const int64_t e = base + (int64_t)m * 32 + lane;
-      const int j = A.cols[e];
-      const double xv = (MODE == 2) ? x[j] : x[(int64_t)B * j + c];
-      return A.vals[(base + (int64_t)m * 32) * (B * B) + (int64_t)(r * B + c) * 32 + lane] * xv;
-    };
-    res[r] = segsum_rt(f, B * len);
-  }
+__device__ __forceinline__ double bsr_row_long(const cprb_sell& A, int64_t base, int lane, int r,
+                                               int len, const double* __restrict__ x) {
+  auto f = [&](int t) -> double {
+    const int m = t / B, c = t - m * B;
+    if (MODE == 2 && c != 0) return 0.0;
+    const int64_t e = base + (int64_t)m * 32 + lane;
+    const int j = __ldg(A.cols + e);
+    const double xv = (MODE == 2) ? __ldg(x + j) : __ldg(x + (int64_t)B * j + c);
+    return __ldg(A.vals + (base + (int64_t)m * 32) * (B * B) + (int64_t)(r * B + c) * 32 + lane) * xv;
+  };
+  return segsum_rt(f, B * len);
 }
 
 template <int B, int MODE>
-__global__ void __launch_bounds__(256) k_bsr(const cprb_sell A, const double* __restrict__ x,
-                                             const double* __restrict__ rhs,
-                                             double* __restrict__ out, int32_t* flag,
-                                             double* __restrict__ sent,
-                                             const int32_t* __restrict__ out_idx) {
+__global__ void __launch_bounds__(BSR_WARPS * 32, 4)
+    k_bsr(const cprb_sell A, const double* __restrict__ x, const double* __restrict__ rhs,
+          double* __restrict__ out, int32_t* flag, double* __restrict__ sent,
+          const int32_t* __restrict__ out_idx) {
   pdl_trigger();
-  pdl_wait();
-  const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int gw = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
-  if (w >= A.nslices) return;
-  const int lid = w * 32 + lane;
-  const int row = A.lane_row[lid];
+  const int s = gw / B;
+  const int r = gw - s * B;
+  if (s >= A.nslices) return;
+  const int lid = s * 32 + lane;
+  const int64_t base = __ldg(A.slice_ptr + s);
+  const int width = (int)((__ldg(A.slice_ptr + s + 1) - base) >> 5);
+  const int row = __ldg(A.lane_row + lid);
+  const int len = row >= 0 ? __ldg(A.lane_len + lid) : 0;
+  pdl_wait();
+  double v;
+  switch (width) {
+    case 0: v = 0.0; break;
+    case 1: v = bsr_row_k<B, MODE, 1>(A, base, lane, r, len, x); break;
+    case 2: v = bsr_row_k<B, MODE, 2>(A, base, lane, r, len, x); break;
+    case 3: v = bsr_row_k<B, MODE, 3>(A, base, lane, r, len, x); break;
+    case 4: v = bsr_row_k<B, MODE, 4>(A, base, lane, r, len, x); break;
+    case 5: v = bsr_row_k<B, MODE, 5>(A, base, lane, r, len, x); break;
+    case 6: v = bsr_row_k<B, MODE, 6>(A, base, lane, r, len, x); break;
+    case 7: v = bsr_row_k<B, MODE, 7>(A, base, lane, r, len, x); break;
+    case 8: v = bsr_row_k<B, MODE, 8>(A, base, lane, r, len, x); break;
+    default: v = bsr_row_long<B, MODE>(A, base, lane, r, len, x); break;
+  }
   if (row < 0) return;
-  const int len = A.lane_len[lid];
-  const int64_t base = A.slice_ptr[w];
-  double res[B];
-  switch (len) {
-    case 0:
-#pragma unroll
-      for (int r = 0; r < B; ++r) res[r] = 0.0;
-      break;
-    case 1: bsr_row_fixed<B, MODE, 1>(A, base, lane, x, res); break;
-    case 2: bsr_row_fixed<B, MODE, 2>(A, base, lane, x, res); break;
-    case 3: bsr_row_fixed<B, MODE, 3>(A, base, lane, x, res); break;
-    case 4: bsr_row_fixed<B, MODE, 4>(A, base, lane, x, res); break;
-    case 5: bsr_row_fixed<B, MODE, 5>(A, base, lane, x, res); break;
-    case 6: bsr_row_fixed<B, MODE, 6>(A, base, lane, x, res); break;
-    case 7: bsr_row_fixed<B, MODE, 7>(A, base, lane, x, res); break;
-    default: bsr_row_generic<B, MODE>(A, base, lane, len, x, res); break;
-  }
-  bool bad = false;
-  const int64_t ob = out_idx ? (int64_t)out_idx[row] : (int64_t)B * row;
-#pragma unroll
-  for (int r = 0; r < B; ++r) {
-    const int64_t o = (int64_t)B * row + r;
-    const double v = (MODE == 0) ? res[r] : rhs[o] - res[r];
-    out[ob + r] = v;
-    bad |= !isfinite(v);
-    if (MODE == 2 && sent) sent[o] = sentinel();
-  }
-  flag_nonfinite(flag, bad);
+  const int64_t o = (int64_t)B * row + r;
+  if (MODE != 0) v = rhs[o] - v;
+  const int64_t ob = out_idx ? (int64_t)out_idx[row] + r : o;
+  out[ob] = v;
+  if (MODE == 2 && sent) sent[o] = sentinel();
+  flag_nonfinite(flag, !isfinite(v));
 }
 
 template <int B, int MODE>
 static void launch_bsr(const cprb_sell& A, const double* x, const double* rhs, double* out,
                        int32_t* flag, double* sent, cudaStream_t st, const int32_t* oi) {
   if (A.nslices <= 0) return;
-  const int threads = 256;
-  const int blocks = (A.nslices * 32 + threads - 1) / threads;
+  const int threads = BSR_WARPS * 32;
+  const int64_t warps = (int64_t)A.nslices * B;
+  const int blocks = (int)((warps + BSR_WARPS - 1) / BSR_WARPS);
   launch_pdl(k_bsr<B, MODE>, blocks, threads, 0, st, A, x, rhs, out, flag, sent, oi);
 }
 
