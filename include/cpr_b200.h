@@ -124,6 +124,23 @@ typedef struct cprb_amg_level {
   double* tmp;                 /* dev work, n (snapshot sweeps) */
 } cprb_amg_level;
 
+/* Device-resident copy of one coarse level for the persistent V-cycle tail
+ * (csrc/amg.cu: k_vtail).  Colour bounds live in the tail_colors table at
+ * color_off: slices[ncolors+1], rows[ncolors+1], snapshot[ncolors]. */
+typedef struct cprb_tail_level {
+  cprb_sell smoother;
+  cprb_sell restrict_op;
+  const double* diag;
+  const int32_t* aggp;
+  double* b;
+  double* x;
+  double* tmp;
+  int32_t n;
+  int32_t ncolors;
+  int32_t color_off;
+  int32_t pad_;
+} cprb_tail_level;
+
 typedef struct cprb_amg {
   int32_t nlevels;                  /* total, including the coarsest */
   const cprb_amg_level* levels;     /* host array, nlevels-1 entries  */
@@ -137,6 +154,12 @@ typedef struct cprb_amg {
   int32_t use_fcg;                  /* K-cycle Krylov flavour */
   double* kwork;                    /* dev work for the K-cycle (see engine) */
   int64_t kwork_len;
+  /* persistent tail: levels >= tail_start (and the coarse solve) run in one
+   * cluster-wide kernel; tail_start >= nlevels-1 disables it. */
+  int32_t tail_start;
+  int32_t tail_ctas;                /* cluster size (1..16) */
+  const cprb_tail_level* tail_levels; /* dev, nlevels-1 entries (index = level) */
+  const int32_t* tail_colors;       /* dev colour table */
 } cprb_amg;
 
 /* Chunked-wavefront plan of one triangular factor (csrc/wave.cu).  Rows are
@@ -208,6 +231,14 @@ int cprb_pgs_scm_pass(const cprb_amg_level* lvl, const double* b, double* x, int
 /* src/amg.py:228-267  z = amg_cycle(h, r); r strided by h->in_stride. */
 int cprb_amg_cycle(const cprb_amg* h, const double* r, double* z, void* stream);
 
+/* Cluster size the persistent V-cycle tail launches with (probed once) and
+ * the probe log. */
+int cprb_vtail_info(int32_t* max_ctas, char* buf, int32_t cap);
+/* Diagnostic: run only the tail kernel, recording %globaltimer at every
+ * phase boundary into dev_log (device, >= 4096 entries). */
+int cprb_vtail_timeline(const cprb_amg* h, const double* r, double* z, uint64_t* dev_log,
+                        void* stream);
+
 /* K-cycle building blocks (the K-cycle recursion, src/amg.py:177-225,
  * :256-263, is driven by the host layer with these device steps). */
 int cprb_coarse_solve(const cprb_amg* h, const double* b, double* x, void* stream);
@@ -218,6 +249,10 @@ int cprb_prolong(const cprb_amg_level* lvl, const double* xc, double* x, void* s
 /* src/ilu.py:196-223  z = U^{-1} L^{-1} r (level-ordered, sync-free). */
 int cprb_bilu_apply(const cprb_bilu* F, const double* r, double* z, double* work_l,
                     void* stream);
+
+/* Diagnostic: record per-step completion times of the wave solves into
+ * dev_log ([2][256 chunks][512 steps] uint64, %globaltimer); NULL = off. */
+int cprb_wave_set_log(uint64_t* dev_log);
 
 /* src/cpr.py:178-186  z = B r (V-cycle pressure stage). */
 int cprb_cpr_apply(const cprb_cpr* P, const double* r, double* z, void* stream);

@@ -38,11 +38,18 @@ class AmgLevel(C.Structure):
                 ("tmp", vp)]
 
 
+class TailLevel(C.Structure):
+    _fields_ = [("smoother", Sell), ("restrict_op", Sell), ("diag", vp), ("aggp", vp), ("b", vp),
+                ("x", vp), ("tmp", vp), ("n", C.c_int32), ("ncolors", C.c_int32),
+                ("color_off", C.c_int32), ("pad_", C.c_int32)]
+
+
 class Amg(C.Structure):
     _fields_ = [("nlevels", C.c_int32), ("levels", C.POINTER(AmgLevel)), ("n_coarse", C.c_int32),
                 ("coarse_inv", vp), ("coarse_b", vp), ("coarse_x", vp), ("perm0", vp),
                 ("in_stride", C.c_int32), ("cycle", C.c_int32), ("use_fcg", C.c_int32),
-                ("kwork", vp), ("kwork_len", C.c_int64)]
+                ("kwork", vp), ("kwork_len", C.c_int64), ("tail_start", C.c_int32),
+                ("tail_ctas", C.c_int32), ("tail_levels", vp), ("tail_colors", vp)]
 
 
 class Wave(C.Structure):
@@ -82,6 +89,9 @@ _SIGS = {
     "cprb_amg_cycle": (C.c_int, [C.POINTER(Amg), vp, vp, vp]),
     "cprb_bilu_apply": (C.c_int, [C.POINTER(Bilu), vp, vp, vp, vp]),
     "cprb_cpr_apply": (C.c_int, [C.POINTER(Cpr), vp, vp, vp]),
+    "cprb_wave_set_log": (C.c_int, [vp]),
+    "cprb_vtail_info": (C.c_int, [i32p, C.c_char_p, C.c_int32]),
+    "cprb_vtail_timeline": (C.c_int, [C.POINTER(Amg), vp, vp, vp, vp]),
     "cprb_coarse_solve": (C.c_int, [C.POINTER(Amg), vp, vp, vp]),
     "cprb_resid_restrict": (C.c_int, [C.POINTER(AmgLevel), vp, vp, vp, vp]),
     "cprb_prolong": (C.c_int, [C.POINTER(AmgLevel), vp, vp, vp]),

@@ -15,6 +15,7 @@ runs on the device.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 from typing import Optional
 
@@ -251,6 +252,9 @@ def _permuted_rows_sell(A, perm: np.ndarray, inv: np.ndarray):
     return D.pack_sell(lane_row, lane_ptr, cols, vals, 1, n)
 
 
+TAIL_ROWS = 0  # levels at most this large run in the persistent tail kernel (0 = off)
+
+
 class DeviceAmg:
     """Device-resident hierarchy: per level the colour-permuted smoother, the
     fused residual/restriction operator, the prolongation map and work
@@ -313,6 +317,42 @@ class DeviceAmg:
         self.desc.cycle = 0
         self.desc.use_fcg = 1 if (h.params.krylov == "fcg" or
                                   (h.params.krylov == "auto" and h.symmetric)) else 0
+        self._build_tail()
+
+    def _build_tail(self):
+        """Device descriptors of the levels handled by the persistent tail
+        kernel (csrc/amg.cu k_vtail): every level with at most TAIL_ROWS rows."""
+        L = self.nlevels
+        self.desc.tail_start = L - 1
+        self.desc.tail_ctas = int(os.environ.get("CPRB_TAIL_CTAS", "16"))
+        if L <= 1:
+            return
+        limit = int(os.environ.get("CPRB_TAIL_ROWS", str(TAIL_ROWS)))
+        ts = L - 1
+        for l in range(L - 1):
+            if self.h.levels[l].A.nrows <= limit:
+                ts = l
+                break
+        if ts >= L - 1:
+            return
+        arr = (N.TailLevel * (L - 1))()
+        table = []
+        for l, dl in enumerate(self.levels):
+            d = dl.desc
+            t = arr[l]
+            t.smoother = d.smoother
+            t.restrict_op = d.restrict_op
+            t.diag, t.aggp, t.b, t.x, t.tmp = d.diag, d.aggp, d.b, d.x, d.tmp
+            t.n, t.ncolors, t.color_off = d.n, d.ncolors, len(table)
+            table.extend(dl.color_slices.tolist())
+            table.extend(dl.color_rows.tolist())
+            table.extend(dl.snapshot.astype(np.int32).tolist())
+        raw = np.frombuffer(bytes(arr), dtype=np.uint8).copy()
+        self.tail_levels = D.upload(raw)
+        self.tail_colors = D.upload(np.asarray(table, dtype=np.int32))
+        self.desc.tail_levels = D.ptr(self.tail_levels)
+        self.desc.tail_colors = D.ptr(self.tail_colors)
+        self.desc.tail_start = ts
 
     # -- V-cycle: one native call ------------------------------------------------
     def vcycle(self, r, z):

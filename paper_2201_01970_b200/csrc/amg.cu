@@ -6,6 +6,8 @@
 // operator stores each aggregate's (<= 2) member rows in adjacent lanes, in
 // the level's ORIGINAL column order, so the fused residual + bincount kernel
 // reproduces `r - spmv(A_l, x)` and `np.bincount` bitwise.
+#include <cstdio>
+#include <string>
 #include <vector>
 
 #include "device.cuh"
@@ -22,6 +24,33 @@ namespace cprb {
 //         and it is stored into b for the rest of the cycle.
 // SCATTER: final value also written to out[perm[i]] (natural order).
 constexpr int SWEEP_PRE = 8;  // entries held in registers across the PDL wait
+
+// continue a GS row sum acc += sum_{m0 <= m < len} a_m x[c_m] in storage
+// order; entries are fetched CH at a time (all loads of a chunk in flight
+// before the first use) so a long coarse-level row costs len/CH dependent
+// round trips instead of len.  x is read through L2 (__ldcg): in the
+// persistent tail it is rewritten between phases by other CTAs.
+template <int CH>
+__device__ __forceinline__ double gs_acc_from(const cprb_sell& S, int64_t base, int m0, int len,
+                                              const double* x, double acc) {
+  for (; m0 < len; m0 += CH) {
+    int c[CH];
+    double v[CH], xv[CH];
+#pragma unroll
+    for (int k = 0; k < CH; ++k)
+      if (m0 + k < len) {
+        c[k] = __ldg(S.cols + base + (int64_t)(m0 + k) * 32);
+        v[k] = __ldg(S.vals + base + (int64_t)(m0 + k) * 32);
+      }
+#pragma unroll
+    for (int k = 0; k < CH; ++k)
+      if (m0 + k < len) xv[k] = __ldcg(x + c[k]);
+#pragma unroll
+    for (int k = 0; k < CH; ++k)
+      if (m0 + k < len) acc = acc + v[k] * xv[k];
+  }
+  return acc;
+}
 
 template <int ZG, int GATHER, int SCATTER>
 __global__ void __launch_bounds__(256)
@@ -64,14 +93,14 @@ __global__ void __launch_bounds__(256)
   } else {
     bi = b[row];
   }
+  double xv[SWEEP_PRE];
+#pragma unroll
+  for (int m = 0; m < SWEEP_PRE; ++m) xv[m] = (m < len) ? xin[colr[m]] : 0.0;
   double acc = 0.0;
 #pragma unroll
   for (int m = 0; m < SWEEP_PRE; ++m)
-    if (m < len) acc = acc + valr[m] * xin[colr[m]];
-  for (int m = SWEEP_PRE; m < len; ++m) {
-    const int64_t e = base + (int64_t)m * 32;
-    acc = acc + __ldg(S.vals + e) * xin[__ldg(S.cols + e)];
-  }
+    if (m < len) acc = acc + valr[m] * xv[m];
+  if (len > SWEEP_PRE) acc = gs_acc_from<8>(S, base, SWEEP_PRE, len, xin, acc);
   const double xn = (bi - acc) / d;
   xout[row] = xn;
   if (SCATTER) sout[pidx] = xn;
@@ -106,15 +135,83 @@ __global__ void k_gs_sequential(const cprb_sell S, int n, const double* diag, co
 
 // residual r_i = b_i - A_l x (row in original column order, reduceat sum)
 // fused with restriction rc[I] = (0 + r_{i1}) + r_{i2}  (np.bincount order).
-constexpr int RR_PRE = 16;
-
-template <int K>
-__device__ __forceinline__ double rr_sum_fixed(const int* colr, const double* valr,
-                                               const double* x) {
-  double e[K];
+// The slice width is warp-uniform; lanes walk it predicated and sum with
+// segsum_masked, so rows of different length keep the warp converged.
+// Streaming form of the reduceat order: a0 + pairwise8(a[1:len]).  Entries are
+// fetched CH (a multiple of 8) at a time; the eight pairwise accumulators are
+// updated group by group, the tree is formed once the complete groups are
+// consumed and the tail is added sequentially, so only r[8] + one chunk are
+// live.  Bit-identical to np.add.reduceat for len <= 129 (no >128 split).
+template <int CH>
+__device__ __forceinline__ double rr_row_stream(const cprb_sell& R, int64_t base, int len,
+                                                const double* x) {
+  static_assert(CH % 8 == 0, "chunk must hold whole groups of 8");
+  if (len <= 0) return 0.0;
+  const int n = len - 1;
+  const int nf = n >= 8 ? (n & ~7) : 0;
+  double a0 = 0.0, s = -0.0, r[8];
 #pragma unroll
-  for (int m = 0; m < K; ++m) e[m] = valr[m] * x[colr[m]];
-  return segsum_fixed<K>(e);
+  for (int k = 0; k < 8; ++k) r[k] = 0.0;
+  for (int p0 = 0; p0 < len; p0 += CH) {  // p = storage position, q = p - 1
+    int c[CH];
+    double v[CH], e[CH];
+#pragma unroll
+    for (int k = 0; k < CH; ++k)
+      if (p0 + k < len) {
+        c[k] = __ldg(R.cols + base + (int64_t)(p0 + k) * 32);
+        v[k] = __ldg(R.vals + base + (int64_t)(p0 + k) * 32);
+      }
+#pragma unroll
+    for (int k = 0; k < CH; ++k) e[k] = (p0 + k < len) ? v[k] * __ldcg(x + c[k]) : 0.0;
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      const int p = p0 + k;
+      if (p >= len) break;
+      if (p == 0) {
+        a0 = e[k];
+        continue;
+      }
+      const int q = p - 1;
+      if (q < nf) {
+        if (q < 8) r[q & 7] = e[k];
+        else r[q & 7] = r[q & 7] + e[k];
+        if (q == nf - 1) s = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+      } else {
+        s = s + e[k];
+      }
+    }
+  }
+  return a0 + s;
+}
+
+__device__ __forceinline__ double rr_row(const cprb_sell& R, int64_t base, int width, int len,
+                                         const double* x) {
+  if (len <= 129) return rr_row_stream<8>(R, base, len, x);
+  auto f = [&](int m) -> double {
+    const int64_t e = base + (int64_t)m * 32;
+    return __ldg(R.vals + e) * __ldcg(x + __ldg(R.cols + e));
+  };
+  return segsum_rt(f, len);
+}
+
+// one warp = one restriction slice (16 aggregates); returns nothing, writes bc
+__device__ __forceinline__ void rr_slice(const cprb_sell& R, int w, int lane, const double* b,
+                                         const double* x, double* bc) {
+  const int lid = w * 32 + lane;
+  const int row = __ldg(R.lane_row + lid);
+  const int len = row >= 0 ? __ldg(R.lane_len + lid) : 0;
+  const int64_t sb = __ldg(R.slice_ptr + w);
+  const int width = (int)((__ldg(R.slice_ptr + w + 1) - sb) >> 5);
+  const int out = ((lane & 1) == 0) ? __ldg(R.agg_out + w * 16 + (lane >> 1)) : -1;
+  double res = 0.0;
+  if (width > 0) {
+    const double t = rr_row(R, sb + lane, width, len, x);
+    if (row >= 0) res = __ldcg(b + row) - t;
+  } else if (row >= 0) {
+    res = __ldcg(b + row) - 0.0;
+  }
+  const double other = __shfl_down_sync(CPRB_FULL, res, 1);
+  if ((lane & 1) == 0 && out >= 0) bc[out] = (0.0 + res) + other;
 }
 
 __global__ void __launch_bounds__(256)
@@ -123,59 +220,9 @@ __global__ void __launch_bounds__(256)
   pdl_trigger();
   const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
-  const bool wok = w < R.nslices;  // warp-uniform
-  const int lid = w * 32 + lane;
-  int row = -1, len = 0, out = -1;
-  int64_t base = 0;
-  int colr[RR_PRE];
-  double valr[RR_PRE];
-  if (wok) {
-    row = __ldg(R.lane_row + lid);
-    len = __ldg(R.lane_len + lid);
-    base = __ldg(R.slice_ptr + w) + lane;
-    if ((lane & 1) == 0) out = __ldg(R.agg_out + w * 16 + (lane >> 1));
-#pragma unroll
-    for (int m = 0; m < RR_PRE; ++m)
-      if (m < len) {
-        colr[m] = __ldg(R.cols + base + (int64_t)m * 32);
-        valr[m] = __ldg(R.vals + base + (int64_t)m * 32);
-      }
-  }
   pdl_wait();
-  if (!wok) return;
-  double res = 0.0;
-  if (row >= 0) {
-    double t;
-    switch (len) {
-      case 0: t = 0.0; break;
-      case 1: t = rr_sum_fixed<1>(colr, valr, x); break;
-      case 2: t = rr_sum_fixed<2>(colr, valr, x); break;
-      case 3: t = rr_sum_fixed<3>(colr, valr, x); break;
-      case 4: t = rr_sum_fixed<4>(colr, valr, x); break;
-      case 5: t = rr_sum_fixed<5>(colr, valr, x); break;
-      case 6: t = rr_sum_fixed<6>(colr, valr, x); break;
-      case 7: t = rr_sum_fixed<7>(colr, valr, x); break;
-      case 8: t = rr_sum_fixed<8>(colr, valr, x); break;
-      case 9: t = rr_sum_fixed<9>(colr, valr, x); break;
-      case 10: t = rr_sum_fixed<10>(colr, valr, x); break;
-      case 11: t = rr_sum_fixed<11>(colr, valr, x); break;
-      case 12: t = rr_sum_fixed<12>(colr, valr, x); break;
-      case 13: t = rr_sum_fixed<13>(colr, valr, x); break;
-      case 14: t = rr_sum_fixed<14>(colr, valr, x); break;
-      case 15: t = rr_sum_fixed<15>(colr, valr, x); break;
-      case 16: t = rr_sum_fixed<16>(colr, valr, x); break;
-      default: {
-        auto f = [&](int m) -> double {
-          const int64_t e = base + (int64_t)m * 32;
-          return __ldg(R.vals + e) * x[__ldg(R.cols + e)];
-        };
-        t = segsum_rt(f, len);
-      }
-    }
-    res = b[row] - t;
-  }
-  const double other = __shfl_down_sync(CPRB_FULL, res, 1);
-  if ((lane & 1) == 0 && out >= 0) bc[out] = (0.0 + res) + other;
+  if (w >= R.nslices) return;
+  rr_slice(R, w, lane, b, x, bc);
 }
 
 // prolongation-correct x += ec[agg]  (src/amg.py:264)
@@ -229,6 +276,230 @@ __global__ void k_scatter(int n, const int32_t* __restrict__ idx, const double* 
 }
 
 static inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
+
+// ---------------------------------------------------------------------------
+// Persistent V-cycle tail.  Levels >= tail_start (their colour sweeps, fused
+// residual + restriction, prolongation) and the coarse solve run in ONE
+// kernel launched as a single thread-block cluster; phases are separated by a
+// cluster barrier (~0.2 us) instead of a dependent kernel launch (~3-5 us).
+// The coarse levels are small (L2 resident after the first touch), so their
+// cost is the number of dependent phases, not bandwidth.  Same arithmetic as
+// the per-colour kernels above (bit-identical results).
+// ---------------------------------------------------------------------------
+constexpr int TAIL_THREADS = 256;
+
+struct TailCtx {
+  int gtid, nthreads, gwarp, nwarps, lane, nctas;
+  unsigned long long* tlog;  // debug timeline (CTA 0 thread 0), nullptr = off
+  int* tn;
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void tail_sync(const TailCtx& t) {
+  if (t.tlog && t.gtid == 0) t.tlog[(*t.tn)++] = gtimer();
+  __syncwarp();
+  if (t.nctas > 1) {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  } else {
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ void tail_colour(const TailCtx& t, const cprb_tail_level& L,
+                                            const int32_t* ct, int k, bool zg, double* x) {
+  const int nc = L.ncolors;
+  const int s0 = ct[k], s1 = ct[k + 1];
+  const int r0 = ct[nc + 1 + k], r1 = ct[nc + 1 + k + 1];
+  const bool snap = ct[2 * (nc + 1) + k] != 0;
+  double* xout = snap ? L.tmp : x;
+  for (int w = s0 + t.gwarp; w < s1; w += t.nwarps) {
+    const int row = r0 + (w - s0) * 32 + t.lane;
+    if (row >= r1) continue;
+    const int lid = w * 32 + t.lane;
+    const int len = zg ? __ldg(L.smoother.lane_len_lo + lid) : __ldg(L.smoother.lane_len + lid);
+    const int64_t base = __ldg(L.smoother.slice_ptr + w) + t.lane;
+    const double acc = gs_acc_from<16>(L.smoother, base, 0, len, x, 0.0);
+    xout[row] = (__ldcg(L.b + row) - acc) / __ldg(L.diag + row);
+  }
+  if (snap) {
+    tail_sync(t);
+    for (int i = r0 + t.gtid; i < r1; i += t.nthreads) x[i] = __ldcg(L.tmp + i);
+  }
+  tail_sync(t);
+}
+
+__device__ __forceinline__ void tail_pass(const TailCtx& t, const cprb_tail_level& L,
+                                          const int32_t* ct, int dir, bool zg) {
+  const int c = L.ncolors;
+  if (c == 1) {  // classic sequential GS (src/smoothers.py:296-299)
+    if (zg) {
+      for (int i = t.gtid; i < L.n; i += t.nthreads) L.x[i] = 0.0;
+      tail_sync(t);
+    }
+    if (t.gtid == 0) {
+      for (int q = 0; q < L.n; ++q) {
+        const int i = dir ? L.n - 1 - q : q;
+        const int w = i >> 5, lane = i & 31;
+        const int len = L.smoother.lane_len[w * 32 + lane];
+        const int64_t base = L.smoother.slice_ptr[w] + lane;
+        double acc = 0.0;
+        for (int m = 0; m < len; ++m) {
+          const int64_t e = base + (int64_t)m * 32;
+          acc = acc + L.smoother.vals[e] * __ldcg(L.x + L.smoother.cols[e]);
+        }
+        L.x[i] = (__ldcg(L.b + i) - acc) / L.diag[i];
+      }
+    }
+    tail_sync(t);
+    return;
+  }
+  for (int q = 0; q < c; ++q) tail_colour(t, L, ct, dir ? c - 1 - q : q, zg, L.x);
+}
+
+__device__ __forceinline__ double dense_row_dot(const double* row, const double* b, int n,
+                                                int lane) {
+  double s = 0.0;
+  for (int c = lane; c < n; c += 32) s = s + __ldg(row + c) * __ldcg(b + c);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s = s + __shfl_xor_sync(CPRB_FULL, s, o);
+  return s;
+}
+
+__global__ void __launch_bounds__(TAIL_THREADS, 1)
+    k_vtail(const cprb_tail_level* __restrict__ lev, const int32_t* __restrict__ colors, int ts,
+            int nl, int n_coarse, const double* __restrict__ coarse_inv, double* coarse_b,
+            double* coarse_x, const double* r, int stride, const int32_t* __restrict__ perm0,
+            double* z, int nctas, unsigned long long* tlog) {
+  TailCtx t;
+  int tn = 0;
+  t.tlog = tlog;
+  t.tn = &tn;
+  if (tlog && t.gtid == 0) tlog[tn++] = gtimer();
+  t.nctas = nctas;
+  t.gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  t.nthreads = gridDim.x * blockDim.x;
+  t.gwarp = t.gtid >> 5;
+  t.nwarps = t.nthreads >> 5;
+  t.lane = threadIdx.x & 31;
+  if (ts == 0) {  // whole cycle in the tail: CPR restriction r[stride * perm]
+    const cprb_tail_level& L = lev[0];
+    for (int i = t.gtid; i < L.n; i += t.nthreads) L.b[i] = r[(int64_t)stride * __ldg(perm0 + i)];
+    tail_sync(t);
+  }
+  for (int l = ts; l < nl - 1; ++l) {
+    const cprb_tail_level& L = lev[l];
+    tail_pass(t, L, colors + L.color_off, 0, true);
+    double* bc = (l + 1 < nl - 1) ? lev[l + 1].b : coarse_b;
+    for (int w = t.gwarp; w < L.restrict_op.nslices; w += t.nwarps)
+      rr_slice(L.restrict_op, w, t.lane, L.b, L.x, bc);
+    tail_sync(t);
+  }
+  for (int w = t.gwarp; w < n_coarse; w += t.nwarps) {
+    const double s = dense_row_dot(coarse_inv + (int64_t)w * n_coarse, coarse_b, n_coarse, t.lane);
+    if (t.lane == 0) coarse_x[w] = s;
+  }
+  tail_sync(t);
+  for (int l = nl - 2; l >= ts; --l) {
+    const cprb_tail_level& L = lev[l];
+    const double* xc = (l + 1 < nl - 1) ? lev[l + 1].x : coarse_x;
+    for (int i = t.gtid; i < L.n; i += t.nthreads) L.x[i] = __ldcg(L.x + i) + __ldcg(xc + __ldg(L.aggp + i));
+    tail_sync(t);
+    tail_pass(t, L, colors + L.color_off, 1, false);
+  }
+  if (ts == 0) {
+    const cprb_tail_level& L = lev[0];
+    for (int i = t.gtid; i < L.n; i += t.nthreads) z[__ldg(perm0 + i)] = __ldcg(L.x + i);
+  }
+}
+
+static int g_tail_max = 0;
+static std::string g_tail_probe;
+
+static void probe_vtail() {
+  static bool probed = false;
+  if (probed) return;
+  probed = true;
+  cudaError_t e0 = cudaFuncSetAttribute(k_vtail, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e0 != cudaSuccess) {
+    g_tail_probe += std::string("nonportable attr: ") + cudaGetErrorString(e0) + "; ";
+    cudaGetLastError();
+  }
+  for (int want : {16, 8, 4, 2}) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(want);
+    cfg.blockDim = dim3(TAIL_THREADS);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = want;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nclus = 0;
+    cudaError_t e = cudaOccupancyMaxActiveClusters(&nclus, k_vtail, &cfg);
+    g_tail_probe += std::to_string(want) + ":" + (e == cudaSuccess ? std::to_string(nclus) : cudaGetErrorString(e)) + " ";
+    cudaGetLastError();
+    if (e == cudaSuccess && nclus > 0) {
+      g_tail_max = want;
+      return;
+    }
+  }
+  g_tail_max = 1;
+}
+
+static int launch_vtail(const cprb_amg& h, const double* r, double* z, cudaStream_t st,
+                        unsigned long long* tlog = nullptr) {
+  static int max_ctas[2] = {0, 0};
+  static bool probed = true;
+  probe_vtail();
+  max_ctas[1] = g_tail_max;
+  if (!probed) {
+    for (int want : {16, 8, 4, 2}) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(want);
+      cfg.blockDim = dim3(TAIL_THREADS);
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = want;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int nclus = 0;
+      if (cudaOccupancyMaxActiveClusters(&nclus, k_vtail, &cfg) == cudaSuccess && nclus > 0) {
+        max_ctas[1] = want;
+        break;
+      }
+      cudaGetLastError();
+    }
+    probed = true;
+  }
+  int g = h.tail_ctas > 0 ? h.tail_ctas : 16;
+  if (g > max_ctas[1]) g = max_ctas[1];
+  if (g < 1) g = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(g);
+  cfg.blockDim = dim3(TAIL_THREADS);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = g;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_vtail, h.tail_levels, h.tail_colors, h.tail_start,
+                                     h.nlevels, h.n_coarse, h.coarse_inv, h.coarse_b, h.coarse_x, r,
+                                     h.in_stride, h.perm0, z, g, tlog);
+  if (e != cudaSuccess)
+    return set_error(CPRB_EDEVICE, std::string("v-cycle tail launch: ") + cudaGetErrorString(e));
+  return check_launch("v-cycle tail");
+}
 
 template <int ZG, int G, int SC>
 static void launch_sweep(const cprb_amg_level& L, int k, double* b, const double* gsrc,
@@ -285,7 +556,9 @@ int amg_vcycle(const cprb_amg& h, const double* r, double* z, cudaStream_t st) {
                                                                      h.coarse_b, z, nullptr);
     return check_launch("coarse-only cycle");
   }
-  for (int l = 0; l < nl - 1; ++l) {
+  const bool tail = h.tail_levels && h.tail_colors && h.tail_start >= 0 && h.tail_start < nl - 1;
+  const int ts = tail ? h.tail_start : nl - 1;
+  for (int l = 0; l < ts; ++l) {
     const cprb_amg_level& L = h.levels[l];
     int rc = pgs_pass(L, L.b, L.x, 0, 1, l == 0 ? r : nullptr, h.in_stride, h.perm0, nullptr, st);
     if (rc) return rc;
@@ -294,9 +567,14 @@ int amg_vcycle(const cprb_amg& h, const double* r, double* z, cudaStream_t st) {
       launch_pdl(k_resid_restrict, nblk((int64_t)L.restrict_op.nslices * 32, 256), 256, 0, st,
                  L.restrict_op, (const double*)L.b, (const double*)L.x, bc);
   }
-  launch_pdl(k_dense_mv, nblk((int64_t)h.n_coarse * 32, 256), 256, 0, st, h.n_coarse,
-             h.coarse_inv, (const double*)h.coarse_b, h.coarse_x, (const int32_t*)nullptr);
-  for (int l = nl - 2; l >= 0; --l) {
+  if (tail) {
+    int rc = launch_vtail(h, r, z, st);
+    if (rc) return rc;
+  } else {
+    launch_pdl(k_dense_mv, nblk((int64_t)h.n_coarse * 32, 256), 256, 0, st, h.n_coarse,
+               h.coarse_inv, (const double*)h.coarse_b, h.coarse_x, (const int32_t*)nullptr);
+  }
+  for (int l = ts - 1; l >= 0; --l) {
     const cprb_amg_level& L = h.levels[l];
     const double* xc = (l + 1 < nl - 1) ? h.levels[l + 1].x : h.coarse_x;
     launch_pdl(k_prolong, nblk(L.n, 256), 256, 0, st, L.n, L.aggp, xc, L.x);
@@ -309,6 +587,20 @@ int amg_vcycle(const cprb_amg& h, const double* r, double* z, cudaStream_t st) {
 }  // namespace cprb
 
 using namespace cprb;
+
+extern "C" int cprb_vtail_timeline(const cprb_amg* h, const double* r, double* z,
+                                   uint64_t* dev_log, void* stream) {
+  return launch_vtail(*h, r, z, (cudaStream_t)stream, (unsigned long long*)dev_log);
+}
+
+extern "C" int cprb_vtail_info(int32_t* max_ctas, char* buf, int32_t cap) {
+  probe_vtail();
+  *max_ctas = g_tail_max;
+  if (buf && cap > 0) {
+    std::snprintf(buf, cap, "%s", g_tail_probe.c_str());
+  }
+  return CPRB_OK;
+}
 
 extern "C" int cprb_pgs_scm_pass(const cprb_amg_level* lvl, const double* b, double* x,
                                  int32_t direction, int32_t zero_guess, void* stream) {

@@ -1,31 +1,43 @@
 // K8 (fast path): chunked-wavefront BILU(0) triangular solves.
 //
-// Rows are split into contiguous chunks whose length is the dependency
-// bandwidth of the factor (one xy-plane for the natural-ordered 7-point
-// grid), so a chunk only depends on the chunk before it (L) / after it (U).
-// One persistent CTA owns a chunk at a time (ticket order = dependency order,
-// so waiting is deadlock free) and walks its rows level by level ("steps",
-// <= 64 rows, one row per thread):
-//   * the step's blocks, column codes and right-hand side arrive in shared
-//     memory through cp.async.bulk (TMA) copies issued DEPTH steps ahead on
-//     mbarriers, so HBM latency is off the critical path;
-//   * a dependency inside the chunk that is < RING steps old is read from a
-//     shared-memory ring; anything else is polled from global memory, where
-//     every result is published with a relaxed store (sentinel = not ready);
-//   * the rest is a __syncthreads per step.
-// The critical path is ~(#levels x smem step) + (#chunks x one L2 hop)
-// instead of #levels x L2 hops.  Arithmetic is the reference's: einsum block
-// products ((p0 + p2) + p1), reduceat row sums (src/ilu.py:97-107, :216-222).
+// Rows are split into contiguous chunks of two dependency bandwidths (two
+// xy-planes for the natural-ordered 7-point grid), so a chunk only depends on
+// the chunk before it (L) / after it (U).  One persistent CTA owns a chunk
+// (ticket order = dependency order, so waiting is deadlock free) and walks
+// its rows level by level ("steps", <= 128 rows):
+//   * a producer warp streams every step's record (blocks, column codes) and
+//     right-hand side into a shared-memory stage ring with cp.async.bulk (TMA)
+//     on full/empty mbarrier pairs, DEPTH steps ahead of the consumers;
+//   * consumer thread t owns row position t of every step.  There is NO
+//     barrier per step: a dependency computed <= DINT steps ago in this chunk
+//     is read from a shared-memory result ring guarded by a per-slot step
+//     flag (release/acquire at CTA scope), so a row starts as soon as its own
+//     inputs exist and neighbouring positions pipeline across steps;
+//   * anything else (the previous chunk, older rows) is polled from global
+//     memory, where every result is published with a relaxed store
+//     (sentinel NaN = not ready).
+// Critical path ~ (#levels x one smem hand-off) + (#chunks x one L2 hop).
+// Arithmetic is the reference's: einsum block products ((p0 + p2) + p1),
+// reduceat row sums (src/ilu.py:97-107, :216-222).
 #include "device.cuh"
 #include "engine.h"
 
 namespace cprb {
 
-constexpr int WAVE_THREADS = 128;  // == wmax of the plan
-constexpr int WAVE_DEPTH = 4;
-constexpr int WAVE_RING = 4;
+constexpr int WAVE_THREADS = 128;  // consumers == wmax of the plan (rows per step)
+constexpr int WAVE_BLOCK = WAVE_THREADS + 32;  // + one producer warp
+constexpr int WAVE_DEPTH = 4;      // stage ring (steps in flight)
+constexpr int WAVE_DINT = 3;       // == ilu.WAVE_DINT: ring-served dependency distance
+constexpr int WAVE_RING = 8;       // result ring; >= DEPTH + DINT (no overwrite while read)
 constexpr int WAVE_KPRE = 3;       // external dependencies prefetched per row
 constexpr int WAVE_META = 1024;    // step metadata staged in shared memory per chunk
+static_assert(WAVE_RING >= WAVE_DEPTH + WAVE_DINT, "result ring too small");
+
+// diagnostic timeline (cprb_wave_set_log): [UPPER][chunk][local step] ->
+// %globaltimer when row position 0 of the step finished; nullptr = off
+__device__ unsigned long long* g_wave_log = nullptr;
+constexpr int WAVE_LOG_STEPS = 512;
+constexpr int WAVE_LOG_CHUNKS = 256;
 
 struct StepMeta {
   int64_t off;      // stream byte offset
@@ -58,6 +70,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ int ld_acquire_s32(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_s32(int* p, int v) {
+  asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n .reg .pred p;\n WAIT_%=:\n"
@@ -71,8 +97,10 @@ struct WaveSmem {
   uint8_t* stage;     // DEPTH * stage_max
   double* rhs;        // DEPTH * rhs_max/8
   double* ring;       // RING * WAVE_THREADS * B
+  int* flag;          // RING * WAVE_THREADS: global step index held by the ring slot
   StepMeta* meta;     // WAVE_META
-  uint64_t* bar;      // DEPTH
+  uint64_t* full;     // DEPTH (TMA landed)
+  uint64_t* empty;    // DEPTH (all consumer warps done with the slot)
   int* chunk;         // 1
 };
 
@@ -117,11 +145,26 @@ __device__ __forceinline__ void wait_block(const double* g, double* v) {
   }
 }
 
+struct RingRef {
+  const double* vals;  // RING * WAVE_THREADS * B
+  const int* flag;     // RING * WAVE_THREADS
+  int k;               // global step index of the row being computed
+};
+
 template <int B>
-__device__ __forceinline__ void dep_value(int code, int m, const double* ring, const double* glob,
+__device__ __forceinline__ void dep_value(int code, int m, const RingRef& ring, const double* glob,
                                           const Pre<B>& p, double* v) {
   if (code < 0) {
-    const double* s = ring + (int64_t)(-code - 1) * B;
+    const int q = -code - 1;
+    const int diff = q / WAVE_THREADS + 1;
+    const int pos = q - (diff - 1) * WAVE_THREADS;
+    const int dstep = ring.k - diff;
+    const int slot = (dstep % WAVE_RING) * WAVE_THREADS + pos;
+    int spins = 0;
+    while (ld_acquire_s32(ring.flag + slot) != dstep) {
+      if (++spins > 64) __nanosleep(8);
+    }
+    const double* s = ring.vals + (int64_t)slot * B;
 #pragma unroll
     for (int c = 0; c < B; ++c) v[c] = s[c];
     return;
@@ -139,7 +182,7 @@ __device__ __forceinline__ void dep_value(int code, int m, const double* ring, c
 
 template <int B, int K>
 __device__ __forceinline__ void wave_rowsum_fixed(const int32_t* codes, const double* vals, int Wp,
-                                                  int t, const double* ring, const double* glob,
+                                                  int t, const RingRef& ring, const double* glob,
                                                   const Pre<B>& pre, double* tsum) {
   double v[K][B];
 #pragma unroll
@@ -160,7 +203,7 @@ __device__ __forceinline__ void wave_rowsum_fixed(const int32_t* codes, const do
 
 template <int B>
 __device__ __forceinline__ void wave_rowsum_generic(const int32_t* codes, const double* vals,
-                                                    int Wp, int t, int len, const double* ring,
+                                                    int Wp, int t, int len, const RingRef& ring,
                                                     const double* glob, const Pre<B>& pre,
                                                     double* tsum) {
 #pragma unroll
@@ -180,49 +223,36 @@ __device__ __forceinline__ void wave_rowsum_generic(const int32_t* codes, const 
 //                rhs order via aux slots, arms y with the sentinel)
 // UPPER = true : y = Uinv (z - sum U y); final = z1 + y
 template <int B, bool UPPER>
-__global__ void __launch_bounds__(WAVE_THREADS, 1)
+__global__ void __launch_bounds__(WAVE_BLOCK, 1)
     k_wave(const cprb_wave W, const double* __restrict__ rhs_steps, double* out_nat,
            double* __restrict__ next_rhs, double* __restrict__ arm, const double* __restrict__ zp,
            double* __restrict__ final_out, int32_t* ticket) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   constexpr int BB = B * B;
   const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const bool producer = warp == WAVE_THREADS / 32;
   const int stage_max = W.stage_max, rhs_max = W.rhs_max;
   WaveSmem S;
   S.stage = smem_raw;
   S.rhs = reinterpret_cast<double*>(smem_raw + (size_t)WAVE_DEPTH * stage_max);
   S.ring = S.rhs + (size_t)WAVE_DEPTH * (rhs_max / 8);
-  S.meta = reinterpret_cast<StepMeta*>(S.ring + (size_t)WAVE_RING * WAVE_THREADS * B);
-  S.bar = reinterpret_cast<uint64_t*>(S.meta + WAVE_META);
-  S.chunk = reinterpret_cast<int*>(S.bar + WAVE_DEPTH);
+  S.flag = reinterpret_cast<int*>(S.ring + (size_t)WAVE_RING * WAVE_THREADS * B);
+  S.meta = reinterpret_cast<StepMeta*>(S.flag + WAVE_RING * WAVE_THREADS);
+  S.full = reinterpret_cast<uint64_t*>(S.meta + WAVE_META);
+  S.empty = S.full + WAVE_DEPTH;
+  S.chunk = reinterpret_cast<int*>(S.empty + WAVE_DEPTH);
   if (tid == 0) {
-    for (int d = 0; d < WAVE_DEPTH; ++d) mbar_init(&S.bar[d], 1);
+    for (int d = 0; d < WAVE_DEPTH; ++d) {
+      mbar_init(&S.full[d], 1);
+      mbar_init(&S.empty[d], WAVE_THREADS / 32);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  for (int i = tid; i < WAVE_RING * WAVE_THREADS; i += blockDim.x) S.flag[i] = -1;
   __syncthreads();
-  uint32_t g = 0;  // steps consumed by this CTA (stage = g % DEPTH, parity = (g / DEPTH) & 1)
-
-  int s0 = 0;
-  bool staged = false;
-  // step metadata: from shared memory when the chunk's steps were staged
-  auto meta = [&](int k) -> StepMeta {
-    if (staged) return S.meta[k - s0];
-    StepMeta m;
-    m.off = W.step_off[k];
-    m.rhs_off = W.rhs_off[k];
-    m.bytes = W.step_bytes[k];
-    m.rhs_bytes = W.rhs_bytes[k];
-    m.w = W.step_w[k];
-    m.k = W.step_k[k];
-    return m;
-  };
-  auto issue = [&](int k, uint32_t gg) {
-    const int st = gg % WAVE_DEPTH;
-    const StepMeta m = meta(k);
-    mbar_expect_tx(&S.bar[st], (uint32_t)(m.bytes + m.rhs_bytes));
-    bulk_g2s(S.stage + (size_t)st * stage_max, W.stream + m.off, m.bytes, &S.bar[st]);
-    bulk_g2s(S.rhs + (size_t)st * (rhs_max / 8), rhs_steps + m.rhs_off, m.rhs_bytes, &S.bar[st]);
-  };
+  uint32_t g = 0;  // steps consumed by this CTA (slot = g % DEPTH, phase = (g / DEPTH) & 1)
+  const RingRef ring0{S.ring, S.flag, 0};
 
   while (true) {
     if (tid == 0) {
@@ -232,11 +262,10 @@ __global__ void __launch_bounds__(WAVE_THREADS, 1)
     }
     __syncthreads();
     const int c = *S.chunk;
-    __syncthreads();  // also: everyone is done with the previous chunk's metadata
     if (c >= W.nchunks) break;
-    s0 = W.chunk_step[c];
+    const int s0 = W.chunk_step[c];
     const int s1 = W.chunk_step[c + 1];
-    staged = (s1 - s0) <= WAVE_META;
+    const bool staged = (s1 - s0) <= WAVE_META;
     if (staged) {
       for (int k = s0 + tid; k < s1; k += blockDim.x) {
         StepMeta m;
@@ -248,99 +277,134 @@ __global__ void __launch_bounds__(WAVE_THREADS, 1)
         m.k = W.step_k[k];
         S.meta[k - s0] = m;
       }
-      __syncthreads();
     }
-    if (tid == 0)
-      for (int k = s0; k < s1 && k < s0 + WAVE_DEPTH; ++k) issue(k, g + (k - s0));
-    Pre<B> pre;
-    // prefetch the first step's cross-chunk dependencies
-    {
-      const int st = g % WAVE_DEPTH;
-      mbar_wait(&S.bar[st], (g / WAVE_DEPTH) & 1);
-      const int w = meta(s0).w;
-      const int Wp = (w + 3) & ~3;
-      const int32_t* rows = reinterpret_cast<const int32_t*>(S.stage + (size_t)st * stage_max);
-      if (tid < w) wave_prefetch<B>(rows + 3 * Wp, Wp, tid, rows[Wp + tid], out_nat, pre);
-    }
-    for (int k = s0; k < s1; ++k, ++g) {
-      const int st = g % WAVE_DEPTH;
-      mbar_wait(&S.bar[st], (g / WAVE_DEPTH) & 1);
-      const uint8_t* blk = S.stage + (size_t)st * stage_max;
-      const StepMeta mk = meta(k);
-      const int w = mk.w, K = mk.k;
-      const int Wp = (w + 3) & ~3;
-      const int32_t* rows = reinterpret_cast<const int32_t*>(blk);
-      const int32_t* lens = rows + Wp;
-      const int32_t* aux = lens + Wp;
-      const int32_t* codes = aux + Wp;
-      // issue the next step's cross-chunk dependency loads now, so their L2
-      // round trip overlaps this step
-      Pre<B> nxt;
-      if (k + 1 < s1) {
-        const int st1 = (g + 1) % WAVE_DEPTH;
-        mbar_wait(&S.bar[st1], ((g + 1) / WAVE_DEPTH) & 1);
-        const int w1 = meta(k + 1).w;
-        const int Wp1 = (w1 + 3) & ~3;
-        const int32_t* r1 = reinterpret_cast<const int32_t*>(S.stage + (size_t)st1 * stage_max);
-        if (tid < w1) wave_prefetch<B>(r1 + 3 * Wp1, Wp1, tid, r1[Wp1 + tid], out_nat, nxt);
-      }
-      const double* vals = reinterpret_cast<const double*>(blk + (size_t)(12 + 4 * K) * Wp);
-      const double* uinv = vals + (size_t)K * BB * Wp;
-      const double* rhs = S.rhs + (size_t)st * (rhs_max / 8);
-      if (tid < w) {
-        const int row = rows[tid];
-        const int len = lens[tid];
-        double z1 = 0.0;
-        if (UPPER && zp) z1 = zp[row];
-        double ts[B];
-        switch (len) {
-          case 0:
-#pragma unroll
-            for (int r = 0; r < B; ++r) ts[r] = 0.0;
-            break;
-          case 1: wave_rowsum_fixed<B, 1>(codes, vals, Wp, tid, S.ring, out_nat, pre, ts); break;
-          case 2: wave_rowsum_fixed<B, 2>(codes, vals, Wp, tid, S.ring, out_nat, pre, ts); break;
-          case 3: wave_rowsum_fixed<B, 3>(codes, vals, Wp, tid, S.ring, out_nat, pre, ts); break;
-          default: wave_rowsum_generic<B>(codes, vals, Wp, tid, len, S.ring, out_nat, pre, ts); break;
-        }
-        double res[B];
-        if constexpr (!UPPER) {
-#pragma unroll
-          for (int r = 0; r < B; ++r) res[r] = rhs[tid * B + r] - ts[r];
-        } else {
-          double d[B], ui[BB];
-#pragma unroll
-          for (int r = 0; r < B; ++r) d[r] = rhs[tid * B + r] - ts[r];
-#pragma unroll
-          for (int e = 0; e < BB; ++e) ui[e] = uinv[(size_t)e * Wp + tid];
-#pragma unroll
-          for (int r = 0; r < B; ++r) res[r] = block_row_dot<B>(&ui[r * B], d);
-        }
-        double* ring_slot = S.ring + ((size_t)(k % WAVE_RING) * WAVE_THREADS + tid) * B;
-#pragma unroll
-        for (int r = 0; r < B; ++r) {
-          ring_slot[r] = res[r];
-          st_relaxed(out_nat + (int64_t)B * row + r, res[r]);
-        }
-        if constexpr (!UPPER) {
-          const int ns = aux[tid];
-#pragma unroll
-          for (int r = 0; r < B; ++r) {
-            next_rhs[(int64_t)ns + r] = res[r];
-            arm[(int64_t)B * row + r] = sentinel();
-          }
-        } else {
-          if (final_out) {
-#pragma unroll
-            for (int r = 0; r < B; ++r)
-              final_out[(int64_t)B * row + r] = zp ? ((r == 0 ? z1 : 0.0) + res[r]) : res[r];
-          }
+    __syncthreads();  // metadata visible; previous chunk fully consumed
+    auto meta = [&](int k) -> StepMeta {
+      if (staged) return S.meta[k - s0];
+      StepMeta m;
+      m.off = W.step_off[k];
+      m.rhs_off = W.rhs_off[k];
+      m.bytes = W.step_bytes[k];
+      m.rhs_bytes = W.rhs_bytes[k];
+      m.w = W.step_w[k];
+      m.k = W.step_k[k];
+      return m;
+    };
+    if (producer) {
+      if ((tid & 31) == 0) {
+        for (int k = s0; k < s1; ++k) {
+          const uint32_t gg = g + (uint32_t)(k - s0);
+          const int st = gg % WAVE_DEPTH;
+          if (gg >= WAVE_DEPTH) mbar_wait(&S.empty[st], ((gg / WAVE_DEPTH) - 1) & 1);
+          const StepMeta m = meta(k);
+          mbar_expect_tx(&S.full[st], (uint32_t)(m.bytes + m.rhs_bytes));
+          bulk_g2s(S.stage + (size_t)st * stage_max, W.stream + m.off, m.bytes, &S.full[st]);
+          bulk_g2s(S.rhs + (size_t)st * (rhs_max / 8), rhs_steps + m.rhs_off, m.rhs_bytes,
+                   &S.full[st]);
         }
       }
-      __syncthreads();  // ring + stage buffer reuse
-      if (tid == 0 && k + WAVE_DEPTH < s1) issue(k + WAVE_DEPTH, g + WAVE_DEPTH);
-      pre = nxt;
+      __syncwarp();
+    } else {
+      Pre<B> pre;
+      {
+        const int st = g % WAVE_DEPTH;
+        mbar_wait(&S.full[st], (g / WAVE_DEPTH) & 1);
+        const int w = meta(s0).w;
+        const int Wp = (w + 3) & ~3;
+        const int32_t* rows = reinterpret_cast<const int32_t*>(S.stage + (size_t)st * stage_max);
+        if (tid < w) wave_prefetch<B>(rows + 3 * Wp, Wp, tid, rows[Wp + tid], out_nat, pre);
+      }
+      for (int k = s0; k < s1; ++k) {
+        const uint32_t gk = g + (uint32_t)(k - s0);
+        const int st = gk % WAVE_DEPTH;
+        mbar_wait(&S.full[st], (gk / WAVE_DEPTH) & 1);
+        const uint8_t* blk = S.stage + (size_t)st * stage_max;
+        const StepMeta mk = meta(k);
+        const int w = mk.w, K = mk.k;
+        const int Wp = (w + 3) & ~3;
+        const int32_t* rows = reinterpret_cast<const int32_t*>(blk);
+        const int32_t* lens = rows + Wp;
+        const int32_t* aux = lens + Wp;
+        const int32_t* codes = aux + Wp;
+        const double* vals = reinterpret_cast<const double*>(blk + (size_t)(12 + 4 * K) * Wp);
+        const double* uinv = vals + (size_t)K * BB * Wp;
+        const double* rhs = S.rhs + (size_t)st * (rhs_max / 8);
+        // issue the next step's cross-chunk dependency loads now (if its
+        // record has landed), so their L2 round trip overlaps this step
+        Pre<B> nxt;
+        if (k + 1 < s1) {
+          const uint32_t g1 = gk + 1;
+          const int st1 = g1 % WAVE_DEPTH;
+          mbar_wait(&S.full[st1], (g1 / WAVE_DEPTH) & 1);
+          const int w1 = meta(k + 1).w;
+          const int Wp1 = (w1 + 3) & ~3;
+          const int32_t* r1 = reinterpret_cast<const int32_t*>(S.stage + (size_t)st1 * stage_max);
+          if (tid < w1) wave_prefetch<B>(r1 + 3 * Wp1, Wp1, tid, r1[Wp1 + tid], out_nat, nxt);
+        }
+        if (tid < w) {
+          RingRef ring = ring0;
+          ring.k = k;
+          const int row = rows[tid];
+          const int len = lens[tid];
+          double z1 = 0.0;
+          if (UPPER && zp) z1 = zp[row];
+          double ts[B];
+          switch (len) {
+            case 0:
+#pragma unroll
+              for (int r = 0; r < B; ++r) ts[r] = 0.0;
+              break;
+            case 1: wave_rowsum_fixed<B, 1>(codes, vals, Wp, tid, ring, out_nat, pre, ts); break;
+            case 2: wave_rowsum_fixed<B, 2>(codes, vals, Wp, tid, ring, out_nat, pre, ts); break;
+            case 3: wave_rowsum_fixed<B, 3>(codes, vals, Wp, tid, ring, out_nat, pre, ts); break;
+            default: wave_rowsum_generic<B>(codes, vals, Wp, tid, len, ring, out_nat, pre, ts); break;
+          }
+          double res[B];
+          if constexpr (!UPPER) {
+#pragma unroll
+            for (int r = 0; r < B; ++r) res[r] = rhs[tid * B + r] - ts[r];
+          } else {
+            double d[B], ui[BB];
+#pragma unroll
+            for (int r = 0; r < B; ++r) d[r] = rhs[tid * B + r] - ts[r];
+#pragma unroll
+            for (int e = 0; e < BB; ++e) ui[e] = uinv[(size_t)e * Wp + tid];
+#pragma unroll
+            for (int r = 0; r < B; ++r) res[r] = block_row_dot<B>(&ui[r * B], d);
+          }
+          const int slot = (k % WAVE_RING) * WAVE_THREADS + tid;
+          double* ring_slot = S.ring + (size_t)slot * B;
+#pragma unroll
+          for (int r = 0; r < B; ++r) ring_slot[r] = res[r];
+          st_release_s32(S.flag + slot, k);
+#pragma unroll
+          for (int r = 0; r < B; ++r) st_relaxed(out_nat + (int64_t)B * row + r, res[r]);
+          if constexpr (!UPPER) {
+            const int ns = aux[tid];
+#pragma unroll
+            for (int r = 0; r < B; ++r) {
+              next_rhs[(int64_t)ns + r] = res[r];
+              arm[(int64_t)B * row + r] = sentinel();
+            }
+          } else {
+            if (final_out) {
+#pragma unroll
+              for (int r = 0; r < B; ++r)
+                final_out[(int64_t)B * row + r] = zp ? ((r == 0 ? z1 : 0.0) + res[r]) : res[r];
+            }
+          }
+        }
+        if (tid == 0 && g_wave_log && c < WAVE_LOG_CHUNKS && k - s0 < WAVE_LOG_STEPS) {
+          unsigned long long tt;
+          asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tt));
+          g_wave_log[((UPPER ? 1 : 0) * WAVE_LOG_CHUNKS + c) * WAVE_LOG_STEPS + (k - s0)] = tt;
+        }
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(&S.empty[st]);  // this warp is done with the slot
+        pre = nxt;
+      }
     }
+    g += (uint32_t)(s1 - s0);
   }
 }
 
@@ -354,7 +418,8 @@ __global__ void k_scatter_slots(int n, int b, const int32_t* __restrict__ slot,
 
 static size_t wave_smem(const cprb_wave& W, int b) {
   return (size_t)WAVE_DEPTH * (W.stage_max + W.rhs_max) + (size_t)WAVE_RING * WAVE_THREADS * b * 8 +
-         sizeof(StepMeta) * WAVE_META + WAVE_DEPTH * 8 + 16;
+         (size_t)WAVE_RING * WAVE_THREADS * 4 + sizeof(StepMeta) * WAVE_META +
+         2 * WAVE_DEPTH * 8 + 16;
 }
 
 template <int B, bool UPPER>
@@ -370,8 +435,8 @@ static int launch_wave(const cprb_wave& W, const double* rhs_steps, double* out_
   const size_t smem = wave_smem(W, B);
   cudaFuncSetAttribute(k_wave<B, UPPER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = W.nchunks < num_sms ? W.nchunks : num_sms;
-  k_wave<B, UPPER><<<grid, WAVE_THREADS, smem, st>>>(W, rhs_steps, out_nat, next_rhs, arm, zp,
-                                                     final_out, ticket);
+  k_wave<B, UPPER><<<grid, WAVE_BLOCK, smem, st>>>(W, rhs_steps, out_nat, next_rhs, arm, zp,
+                                                   final_out, ticket);
   return check_launch("wave solve");
 }
 
@@ -393,6 +458,16 @@ int wave_solve(const cprb_bilu& F, const double* rhsL, double* zl, double* zu_rh
   }
   return rc;
 }
+
+}  // namespace cprb
+
+extern "C" int cprb_wave_set_log(uint64_t* dev_log) {
+  unsigned long long* p = (unsigned long long*)dev_log;
+  cudaMemcpyToSymbol(cprb::g_wave_log, &p, sizeof(p));
+  return cprb::check_launch("wave log");
+}
+
+namespace cprb {
 
 int wave_scatter_rhs(const cprb_bilu& F, const double* r, double* rhsL, cudaStream_t st) {
   k_scatter_slots<<<(F.n + 255) / 256, 256, 0, st>>>(F.n, F.b, F.l_slot, r, rhsL);

@@ -152,7 +152,7 @@ def _level_sell(T: BlockCsrMatrix, sched: LevelSchedule, b: int, uinv=None):
 
 
 WAVE_WMAX = 128         # rows per step == threads per CTA (csrc/wave.cu)
-WAVE_RING = 4           # steps kept in the shared-memory ring
+WAVE_DINT = 3           # dependencies at most this many steps back are read from shared memory
 WAVE_STAGE_CAP = 40960  # bytes per streamed step
 WAVE_BANDS = 2          # dependency bandwidths (xy-planes) per chunk
 
@@ -229,8 +229,9 @@ def wave_plan(T: BlockCsrMatrix, sched: LevelSchedule, b: int, upper: bool, uinv
     m = ent - ptr[rows_of]
     ri = rows_of
     dep = cols
-    internal = (chunk[dep] == chunk[ri]) & (row_step[ri] - row_step[dep] < WAVE_RING)
-    slot = (row_step[dep] % WAVE_RING) * WAVE_WMAX + row_pos[dep]
+    diff = row_step[ri] - row_step[dep]
+    internal = (chunk[dep] == chunk[ri]) & (diff >= 1) & (diff <= WAVE_DINT)
+    slot = (diff - 1) * WAVE_WMAX + row_pos[dep]
     code = np.where(internal, -(slot + 1), dep)
     e_st = row_step[ri]
     e_Wp = Wp[e_st]

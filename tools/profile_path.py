@@ -9,6 +9,7 @@ from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_2201_01970_b200 as P  # noqa: E402
@@ -39,6 +40,49 @@ def main():
         "vcycle": lambda: Bd.amg.vcycle(bd, zp),
         "solve": lambda: P.gmres_solve(A, bd, None, B, cfg.gmres_params()),
     }
+    import ctypes as C
+    from paper_2201_01970_b200 import _native as N
+    mx = C.c_int32(0)
+    buf = C.create_string_buffer(512)
+    N.lib().cprb_vtail_info(C.byref(mx), buf, 512)
+    print("vtail cluster:", mx.value, buf.value.decode(), "tail_start", Bd.amg.desc.tail_start)
+    if a.what == "tailtl":
+        t = torch
+        log = t.zeros(4096, dtype=t.int64, device="cuda")
+        for rep in range(3):
+            log.zero_()
+            N.lib().cprb_vtail_timeline(C.byref(Bd.amg.desc), D.ptr(bd), D.ptr(zp), D.ptr(log), D.stream())
+            t.cuda.synchronize()
+        L = log.cpu().numpy()
+        L = L[L > 0]
+        d = np.diff(L) / 1e3
+        print("tail phases", len(d), "total us", (L[-1] - L[0]) / 1e3)
+        print(" ".join(f"{v:.2f}" for v in d))
+        return
+    if a.what == "wavetl":
+        t = torch
+        log = t.zeros(2 * 256 * 512, dtype=t.int64, device="cuda")
+        N.lib().cprb_wave_set_log(D.ptr(log))
+        for rep in range(3):
+            log.zero_()
+            Bd.bilu.apply(bd, z)
+            t.cuda.synchronize()
+        N.lib().cprb_wave_set_log(None)
+        L = log.cpu().numpy().reshape(2, 256, 512)
+        t0 = L[L > 0].min()
+        for u in range(2):
+            nch = int((L[u, :, 0] > 0).sum())
+            print(("U" if u else "L"), "chunks", nch)
+            for c in list(range(min(nch, 4))) + [nch // 2, nch - 1]:
+                row = L[u, c]
+                row = row[row > 0]
+                d = np.diff(row)
+                print(f" chunk {c}: start {(row[0]-t0)/1e3:.1f} end {(row[-1]-t0)/1e3:.1f} us, steps {row.size},"
+                      f" median step {np.median(d)/1e3:.3f} us, max step {d.max()/1e3:.2f}")
+            # lag between consecutive chunks at equal local step 100
+            lag = [(L[u, c, 100] - L[u, c - 1, 100]) / 1e3 for c in range(1, nch) if L[u, c, 100] > 0]
+            print(" lag@step100 median", np.median(lag), "first", lag[:5])
+        return
     fn = ops[a.what]
     fn()
     torch.cuda.synchronize()
