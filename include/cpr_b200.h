@@ -122,6 +122,9 @@ typedef struct cprb_amg_level {
   double* b;                   /* dev work, n */
   double* x;                   /* dev work, n */
   double* tmp;                 /* dev work, n (snapshot sweeps) */
+  const int32_t* color_width;  /* host|NULL, 2*ncolors: max lane_len, max lane_len_lo per colour */
+  int32_t restrict_width;      /* max row length of restrict_op (0 = unknown) */
+  int32_t pad_;
 } cprb_amg_level;
 
 /* Device-resident copy of one coarse level for the persistent V-cycle tail
@@ -234,6 +237,9 @@ int cprb_amg_cycle(const cprb_amg* h, const double* r, double* z, void* stream);
 /* Cluster size the persistent V-cycle tail launches with (probed once) and
  * the probe log. */
 int cprb_vtail_info(int32_t* max_ctas, char* buf, int32_t cap);
+/* Diagnostic: V-cycle kernel timeline ({kind, start, after-wait, end} u64
+ * per launch, %globaltimer, <= 4096 launches); resets the counter; NULL = off. */
+int cprb_amg_set_log(uint64_t* dev_log);
 /* Diagnostic: run only the tail kernel, recording %globaltimer at every
  * phase boundary into dev_log (device, >= 4096 entries). */
 int cprb_vtail_timeline(const cprb_amg* h, const double* r, double* z, uint64_t* dev_log,

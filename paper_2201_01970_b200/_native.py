@@ -35,7 +35,8 @@ class AmgLevel(C.Structure):
     _fields_ = [("n", C.c_int32), ("ncolors", C.c_int32), ("color_slices", i32p),
                 ("color_rows", i32p), ("color_snapshot", u8p), ("smoother", Sell),
                 ("diag", vp), ("restrict_op", Sell), ("aggp", vp), ("b", vp), ("x", vp),
-                ("tmp", vp)]
+                ("tmp", vp), ("color_width", i32p), ("restrict_width", C.c_int32),
+                ("pad_", C.c_int32)]
 
 
 class TailLevel(C.Structure):
@@ -90,6 +91,7 @@ _SIGS = {
     "cprb_bilu_apply": (C.c_int, [C.POINTER(Bilu), vp, vp, vp, vp]),
     "cprb_cpr_apply": (C.c_int, [C.POINTER(Cpr), vp, vp, vp]),
     "cprb_wave_set_log": (C.c_int, [vp]),
+    "cprb_amg_set_log": (C.c_int, [vp]),
     "cprb_vtail_info": (C.c_int, [i32p, C.c_char_p, C.c_int32]),
     "cprb_vtail_timeline": (C.c_int, [C.POINTER(Amg), vp, vp, vp, vp]),
     "cprb_coarse_solve": (C.c_int, [C.POINTER(Amg), vp, vp, vp]),

@@ -291,6 +291,7 @@ class DeviceAmg:
             R = D.SellDev(_restriction_sell(lvl.A, lvl.aggregates, na, invs[l], invs[l + 1]))
             aggp = D.upload(invs[l + 1][lvl.aggregates[perms[l]]].astype(np.int32))
             dl.desc.restrict_op = R.desc
+            dl.desc.restrict_width = int(R.host.lane_len.max()) if R.host.lane_len.size else 0
             dl.desc.aggp = D.ptr(aggp)
             self.levels.append(dl)
             self.restrict.append(R)

@@ -15,6 +15,8 @@
 
 namespace cprb {
 
+static inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
+
 // PGS-SCM colour update (src/smoothers.py:106-115):
 //   x_i = (b_i - sum_{stored off-diagonals, ascending permuted col} a_ij x_j) / d_i
 // ZG: zero initial guess -> only the prefix of entries whose columns precede
@@ -23,7 +25,39 @@ namespace cprb {
 // GATHER: b_i = src[stride * perm[i]] (level-0 CPR restriction, src/cpr.py:132)
 //         and it is stored into b for the rest of the cycle.
 // SCATTER: final value also written to out[perm[i]] (natural order).
-constexpr int SWEEP_PRE = 8;  // entries held in registers across the PDL wait
+// SWEEP_PRE (template): entries held in registers across the PDL wait,
+// chosen per colour from its widest row so the whole static part of a row is
+// fetched while the previous kernel still runs.
+
+// diagnostic V-cycle timeline (cprb_amg_set_log): per launch, block 0 thread 0
+// records {kind, start, after pdl_wait, end} as %globaltimer; nullptr = off
+__device__ unsigned long long* g_amg_log = nullptr;
+__device__ int g_amg_log_n = 0;
+constexpr int AMG_LOG_CAP = 4096;
+
+struct AmgMark {
+  int idx = -1;
+  __device__ __forceinline__ static unsigned long long now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+  }
+  __device__ __forceinline__ void start(int kind) {
+    if (g_amg_log && blockIdx.x == 0 && threadIdx.x == 0) {
+      idx = atomicAdd(&g_amg_log_n, 1);
+      if (idx < AMG_LOG_CAP) {
+        g_amg_log[4 * idx] = (unsigned long long)kind;
+        g_amg_log[4 * idx + 1] = now();
+      }
+    }
+  }
+  __device__ __forceinline__ void waited() {
+    if (idx >= 0 && idx < AMG_LOG_CAP) g_amg_log[4 * idx + 2] = now();
+  }
+  __device__ __forceinline__ void end() {
+    if (idx >= 0 && idx < AMG_LOG_CAP) g_amg_log[4 * idx + 3] = now();
+  }
+};
 
 // continue a GS row sum acc += sum_{m0 <= m < len} a_m x[c_m] in storage
 // order; entries are fetched CH at a time (all loads of a chunk in flight
@@ -52,13 +86,15 @@ __device__ __forceinline__ double gs_acc_from(const cprb_sell& S, int64_t base, 
   return acc;
 }
 
-template <int ZG, int GATHER, int SCATTER>
+template <int ZG, int GATHER, int SCATTER, int SWEEP_PRE>
 __global__ void __launch_bounds__(256)
     k_sweep(const cprb_sell S, int s0, int s1, int r0, int r1, const double* __restrict__ diag,
             double* b, const double* __restrict__ gsrc, int gstride,
             const int32_t* __restrict__ perm, const double* xin, double* xout,
             double* __restrict__ sout) {
   pdl_trigger();
+  AmgMark mk;
+  mk.start(1 + ZG);
   const int w = s0 + (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   // colours are contiguous row ranges padded to whole slices: the row is
@@ -85,6 +121,7 @@ __global__ void __launch_bounds__(256)
       }
   }
   pdl_wait();
+  mk.waited();
   if (!active) return;
   double bi;
   if (GATHER) {
@@ -104,6 +141,7 @@ __global__ void __launch_bounds__(256)
   const double xn = (bi - acc) / d;
   xout[row] = xn;
   if (SCATTER) sout[pidx] = xn;
+  mk.end();
 }
 
 __global__ void k_copy_rows(const cprb_sell S, int s0, int s1, const double* src, double* dst) {
@@ -214,25 +252,80 @@ __device__ __forceinline__ void rr_slice(const cprb_sell& R, int w, int lane, co
   if ((lane & 1) == 0 && out >= 0) bc[out] = (0.0 + res) + other;
 }
 
+// standalone launch: the static part of the slice (columns, values, output
+// slots) is fetched before the PDL wait; rows longer than PRE fall back to
+// the streaming sum.
+template <int PRE>
 __global__ void __launch_bounds__(256)
     k_resid_restrict(const cprb_sell R, const double* __restrict__ b,
                      const double* __restrict__ x, double* __restrict__ bc) {
   pdl_trigger();
+  AmgMark mk;
+  mk.start(3);
   const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
+  const bool wok = w < R.nslices;  // warp-uniform
+  int row = -1, len = 0, out = -1;
+  int64_t base = 0;
+  int c[PRE];
+  double v[PRE];
+  if (wok) {
+    const int lid = w * 32 + lane;
+    row = __ldg(R.lane_row + lid);
+    len = row >= 0 ? __ldg(R.lane_len + lid) : 0;
+    base = __ldg(R.slice_ptr + w) + lane;
+    if ((lane & 1) == 0) out = __ldg(R.agg_out + w * 16 + (lane >> 1));
+#pragma unroll
+    for (int m = 0; m < PRE; ++m)
+      if (m < len) {
+        c[m] = __ldg(R.cols + base + (int64_t)m * 32);
+        v[m] = __ldg(R.vals + base + (int64_t)m * 32);
+      }
+  }
   pdl_wait();
-  if (w >= R.nslices) return;
-  rr_slice(R, w, lane, b, x, bc);
+  mk.waited();
+  if (!wok) return;
+  double res = 0.0;
+  if (row >= 0) {
+    double t;
+    if (len <= PRE) {
+      double e[PRE];
+#pragma unroll
+      for (int m = 0; m < PRE; ++m) e[m] = (m < len) ? v[m] * __ldcg(x + c[m]) : 0.0;
+      t = segsum_masked<PRE>(e, len);
+    } else {
+      t = rr_row(R, base, 0, len, x);
+    }
+    res = __ldcg(b + row) - t;
+  }
+  const double other = __shfl_down_sync(CPRB_FULL, res, 1);
+  if ((lane & 1) == 0 && out >= 0) bc[out] = (0.0 + res) + other;
+  mk.end();
+}
+
+static void launch_rr(const cprb_amg_level& L, const double* b, const double* x, double* bc,
+                      cudaStream_t st) {
+  const cprb_sell& R = L.restrict_op;
+  if (R.nslices <= 0) return;
+  const int grid = nblk((int64_t)R.nslices * 32, 256);
+  const int wdt = L.restrict_width > 0 ? L.restrict_width : 32;
+  if (wdt <= 8) launch_pdl(k_resid_restrict<8>, grid, 256, 0, st, R, b, x, bc);
+  else if (wdt <= 16) launch_pdl(k_resid_restrict<16>, grid, 256, 0, st, R, b, x, bc);
+  else launch_pdl(k_resid_restrict<32>, grid, 256, 0, st, R, b, x, bc);
 }
 
 // prolongation-correct x += ec[agg]  (src/amg.py:264)
 __global__ void k_prolong(int n, const int32_t* __restrict__ aggp, const double* __restrict__ xc,
                           double* __restrict__ x) {
   pdl_trigger();
+  AmgMark mk;
+  mk.start(4);
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int a = i < n ? __ldg(aggp + i) : 0;
   pdl_wait();
+  mk.waited();
   if (i < n) x[i] = x[i] + xc[a];
+  mk.end();
 }
 
 // coarsest solve: x = inv(A_L) b, one warp per row, fixed lane/shuffle order
@@ -274,8 +367,6 @@ __global__ void k_scatter(int n, const int32_t* __restrict__ idx, const double* 
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) dst[idx ? idx[i] : i] = src[i];
 }
-
-static inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
 // ---------------------------------------------------------------------------
 // Persistent V-cycle tail.  Levels >= tail_start (their colour sweeps, fused
@@ -508,9 +599,16 @@ static void launch_sweep(const cprb_amg_level& L, int k, double* b, const double
   const int s0 = L.color_slices[k], s1 = L.color_slices[k + 1];
   if (s1 <= s0) return;
   const int threads = (s1 - s0) * 32 >= 256 ? 256 : 128;
-  launch_pdl(k_sweep<ZG, G, SC>, nblk((int64_t)(s1 - s0) * 32, threads), threads, 0, st,
-             L.smoother, s0, s1, L.color_rows[k], L.color_rows[k + 1], L.diag, b, gsrc, gstride,
-             perm, xin, xout, sout);
+  const int width = L.color_width ? L.color_width[2 * k + (ZG ? 1 : 0)] : 8;
+  const int grid = nblk((int64_t)(s1 - s0) * 32, threads);
+  auto go = [&](auto kern) {
+    launch_pdl(kern, grid, threads, 0, st, L.smoother, s0, s1, L.color_rows[k],
+               L.color_rows[k + 1], L.diag, b, gsrc, gstride, perm, xin, xout, sout);
+  };
+  if (width <= 4) go(k_sweep<ZG, G, SC, 4>);
+  else if (width <= 8) go(k_sweep<ZG, G, SC, 8>);
+  else if (width <= 16) go(k_sweep<ZG, G, SC, 16>);
+  else go(k_sweep<ZG, G, SC, 32>);
 }
 
 int pgs_pass(const cprb_amg_level& L, const double* b_in, double* x, int dir, int zero_guess,
@@ -563,9 +661,7 @@ int amg_vcycle(const cprb_amg& h, const double* r, double* z, cudaStream_t st) {
     int rc = pgs_pass(L, L.b, L.x, 0, 1, l == 0 ? r : nullptr, h.in_stride, h.perm0, nullptr, st);
     if (rc) return rc;
     double* bc = (l + 1 < nl - 1) ? h.levels[l + 1].b : h.coarse_b;
-    if (L.restrict_op.nslices > 0)
-      launch_pdl(k_resid_restrict, nblk((int64_t)L.restrict_op.nslices * 32, 256), 256, 0, st,
-                 L.restrict_op, (const double*)L.b, (const double*)L.x, bc);
+    launch_rr(L, L.b, L.x, bc, st);
   }
   if (tail) {
     int rc = launch_vtail(h, r, z, st);
@@ -587,6 +683,14 @@ int amg_vcycle(const cprb_amg& h, const double* r, double* z, cudaStream_t st) {
 }  // namespace cprb
 
 using namespace cprb;
+
+extern "C" int cprb_amg_set_log(uint64_t* dev_log) {
+  unsigned long long* p = (unsigned long long*)dev_log;
+  int zero = 0;
+  cudaMemcpyToSymbol(cprb::g_amg_log, &p, sizeof(p));
+  cudaMemcpyToSymbol(cprb::g_amg_log_n, &zero, sizeof(zero));
+  return check_launch("amg log");
+}
 
 extern "C" int cprb_vtail_timeline(const cprb_amg* h, const double* r, double* z,
                                    uint64_t* dev_log, void* stream) {
@@ -617,9 +721,7 @@ extern "C" int cprb_coarse_solve(const cprb_amg* h, const double* b, double* x, 
 
 extern "C" int cprb_resid_restrict(const cprb_amg_level* L, const double* b, const double* x,
                                    double* bc, void* stream) {
-  if (L->restrict_op.nslices <= 0) return CPRB_OK;
-  k_resid_restrict<<<nblk((int64_t)L->restrict_op.nslices * 32, 256), 256, 0, (cudaStream_t)stream>>>(
-      L->restrict_op, b, x, bc);
+  launch_rr(*L, b, x, bc, (cudaStream_t)stream);
   return check_launch("resid restrict");
 }
 

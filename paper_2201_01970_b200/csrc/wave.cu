@@ -219,6 +219,104 @@ __device__ __forceinline__ void wave_rowsum_generic(const int32_t* codes, const 
   }
 }
 
+__device__ __forceinline__ int lds_s32(uint32_t a) {
+  int v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ int lds_acquire_s32(uint32_t a) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_f64(uint32_t a, double v) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void sts_release_s32(uint32_t a, int v) {
+  asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+// One row of a step with at most K (<= WAVE_KPRE) dependencies, all operands
+// addressed explicitly in shared memory (no generic loads, no local memory).
+// Returns the row's result in res[B].
+template <int B, bool UPPER, int K>
+__device__ __forceinline__ void lean_row(uint32_t sblk, uint32_t srhs, uint32_t sring,
+                                         uint32_t sflag, int Wp, int t, int k, int len,
+                                         const double* glob, const Pre<B>& pre, double* res) {
+  constexpr int BB = B * B;
+  constexpr int KA = K > 0 ? K : 1;  // array extent
+  const uint32_t a_codes = sblk + 12u * Wp;
+  const uint32_t a_vals = sblk + (uint32_t)(12 + 4 * K) * Wp;
+  int code[KA];
+  double mv[KA][BB];
+#pragma unroll
+  for (int m = 0; m < K; ++m) {
+    code[m] = (m < len) ? lds_s32(a_codes + 4u * (m * Wp + t)) : 0;
+#pragma unroll
+    for (int e = 0; e < BB; ++e)
+      mv[m][e] = (m < len) ? lds_f64(a_vals + 8u * ((m * BB + e) * Wp + t)) : 0.0;
+  }
+  double rh[B];
+#pragma unroll
+  for (int r = 0; r < B; ++r) rh[r] = lds_f64(srhs + 8u * (t * B + r));
+  double ui[UPPER ? BB : 1];
+  if constexpr (UPPER) {
+    const uint32_t a_ui = a_vals + 8u * (K * BB * Wp);
+#pragma unroll
+    for (int e = 0; e < BB; ++e) ui[e] = lds_f64(a_ui + 8u * (e * Wp + t));
+  }
+  double dv[KA][B];
+#pragma unroll
+  for (int m = 0; m < K; ++m) {
+    if (m < len) {
+      const int cd = code[m];
+      if (cd < 0) {
+        const int q = -cd - 1;
+        const int diff = q / WAVE_THREADS + 1;
+        const int pos = q - (diff - 1) * WAVE_THREADS;
+        const int dstep = k - diff;
+        const uint32_t slot = (uint32_t)((dstep % WAVE_RING) * WAVE_THREADS + pos);
+        while (lds_acquire_s32(sflag + 4u * slot) != dstep) {
+        }
+#pragma unroll
+        for (int c = 0; c < B; ++c) dv[m][c] = lds_f64(sring + 8u * (slot * B + c));
+      } else {
+#pragma unroll
+        for (int c = 0; c < B; ++c) dv[m][c] = pre.v[m][c];
+        wait_block<B>(glob + (int64_t)B * cd, dv[m]);
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < B; ++c) dv[m][c] = 0.0;
+    }
+  }
+  if constexpr (K > 0) {
+#pragma unroll
+    for (int r = 0; r < B; ++r) {
+      double p[K];
+#pragma unroll
+      for (int m = 0; m < K; ++m) p[m] = block_row_dot<B>(&mv[m][r * B], dv[m]);
+      const double ts = segsum_masked<K>(p, len);
+      rh[r] = rh[r] - ts;
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < B; ++r) rh[r] = rh[r] - 0.0;
+  }
+  if constexpr (UPPER) {
+#pragma unroll
+    for (int r = 0; r < B; ++r) res[r] = block_row_dot<B>(&ui[r * B], rh);
+  } else {
+#pragma unroll
+    for (int r = 0; r < B; ++r) res[r] = rh[r];
+  }
+}
+
 // UPPER = false: z = r - sum L z   (publishes z, copies z into the U plan's
 //                rhs order via aux slots, arms y with the sentinel)
 // UPPER = true : y = Uinv (z - sum U y); final = z1 + y
@@ -253,6 +351,8 @@ __global__ void __launch_bounds__(WAVE_BLOCK, 1)
   __syncthreads();
   uint32_t g = 0;  // steps consumed by this CTA (slot = g % DEPTH, phase = (g / DEPTH) & 1)
   const RingRef ring0{S.ring, S.flag, 0};
+  const uint32_t sring = smem_u32(S.ring);
+  const uint32_t sflag = smem_u32(S.flag);
 
   while (true) {
     if (tid == 0) {
@@ -305,6 +405,8 @@ __global__ void __launch_bounds__(WAVE_BLOCK, 1)
       }
       __syncwarp();
     } else {
+      long long cyc[5] = {0, 0, 0, 0, 0};
+      long long tlast = clock64();
       Pre<B> pre;
       {
         const int st = g % WAVE_DEPTH;
@@ -317,7 +419,17 @@ __global__ void __launch_bounds__(WAVE_BLOCK, 1)
       for (int k = s0; k < s1; ++k) {
         const uint32_t gk = g + (uint32_t)(k - s0);
         const int st = gk % WAVE_DEPTH;
+        const bool tl = g_wave_log != nullptr;
+        auto tmark = [&](int which) {
+          if (tl) {
+            const long long now = clock64();
+            if (which > 0) cyc[which - 1] += now - tlast;
+            tlast = now;
+          }
+        };
+        tmark(0);
         mbar_wait(&S.full[st], (gk / WAVE_DEPTH) & 1);
+        tmark(1);
         const uint8_t* blk = S.stage + (size_t)st * stage_max;
         const StepMeta mk = meta(k);
         const int w = mk.w, K = mk.k;
@@ -341,7 +453,44 @@ __global__ void __launch_bounds__(WAVE_BLOCK, 1)
           const int32_t* r1 = reinterpret_cast<const int32_t*>(S.stage + (size_t)st1 * stage_max);
           if (tid < w1) wave_prefetch<B>(r1 + 3 * Wp1, Wp1, tid, r1[Wp1 + tid], out_nat, nxt);
         }
-        if (tid < w) {
+        tmark(2);
+        if (tid < w && K <= WAVE_KPRE) {
+          // lean path (all rows of 7-point-type factors)
+          const uint32_t sblk = smem_u32(blk);
+          const uint32_t srhs = smem_u32(rhs);
+          const int row = lds_s32(sblk + 4u * tid);
+          const int len = lds_s32(sblk + 4u * (Wp + tid));
+          const int ns = UPPER ? 0 : lds_s32(sblk + 4u * (2 * Wp + tid));
+          double z1 = 0.0;
+          if (UPPER && zp) z1 = zp[row];
+          double res[B];
+          switch (K) {
+            case 0: lean_row<B, UPPER, 0>(sblk, srhs, sring, sflag, Wp, tid, k, len, out_nat, pre, res); break;
+            case 1: lean_row<B, UPPER, 1>(sblk, srhs, sring, sflag, Wp, tid, k, len, out_nat, pre, res); break;
+            case 2: lean_row<B, UPPER, 2>(sblk, srhs, sring, sflag, Wp, tid, k, len, out_nat, pre, res); break;
+            default: lean_row<B, UPPER, 3>(sblk, srhs, sring, sflag, Wp, tid, k, len, out_nat, pre, res); break;
+          }
+          tmark(3);
+          const uint32_t slot = (uint32_t)((k % WAVE_RING) * WAVE_THREADS + tid);
+#pragma unroll
+          for (int r = 0; r < B; ++r) sts_f64(sring + 8u * (slot * B + r), res[r]);
+          sts_release_s32(sflag + 4u * slot, k);
+#pragma unroll
+          for (int r = 0; r < B; ++r) st_relaxed(out_nat + (int64_t)B * row + r, res[r]);
+          if constexpr (!UPPER) {
+#pragma unroll
+            for (int r = 0; r < B; ++r) {
+              next_rhs[(int64_t)ns + r] = res[r];
+              arm[(int64_t)B * row + r] = sentinel();
+            }
+          } else {
+            if (final_out) {
+#pragma unroll
+              for (int r = 0; r < B; ++r)
+                final_out[(int64_t)B * row + r] = zp ? ((r == 0 ? z1 : 0.0) + res[r]) : res[r];
+            }
+          }
+        } else if (tid < w) {
           RingRef ring = ring0;
           ring.k = k;
           const int row = rows[tid];
@@ -372,6 +521,7 @@ __global__ void __launch_bounds__(WAVE_BLOCK, 1)
 #pragma unroll
             for (int r = 0; r < B; ++r) res[r] = block_row_dot<B>(&ui[r * B], d);
           }
+          tmark(3);
           const int slot = (k % WAVE_RING) * WAVE_THREADS + tid;
           double* ring_slot = S.ring + (size_t)slot * B;
 #pragma unroll
@@ -399,9 +549,17 @@ __global__ void __launch_bounds__(WAVE_BLOCK, 1)
           asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tt));
           g_wave_log[((UPPER ? 1 : 0) * WAVE_LOG_CHUNKS + c) * WAVE_LOG_STEPS + (k - s0)] = tt;
         }
+        tmark(4);
         __syncwarp();
         if ((tid & 31) == 0) mbar_arrive(&S.empty[st]);  // this warp is done with the slot
         pre = nxt;
+        tmark(5);
+      }
+      if (g_wave_log && c < WAVE_LOG_CHUNKS && tid < 128) {
+        // cycles per phase summed over the chunk, slot [UPPER][200 + phase][chunk*... ] tid-major
+        for (int q = 0; q < 5; ++q)
+          g_wave_log[((UPPER ? 1 : 0) * WAVE_LOG_CHUNKS + 200 + q) * WAVE_LOG_STEPS + (c % 4) * 128 + tid] =
+              (unsigned long long)cyc[q];
       }
     }
     g += (uint32_t)(s1 - s0);

@@ -140,6 +140,17 @@ class DeviceSmootherLevel:
         self.desc.color_slices = N.p32(self.color_slices)
         self.desc.color_rows = N.p32(self.color_rows)
         self.desc.color_snapshot = self.snapshot.ctypes.data_as(N.u8p)
+        # per colour: max row length, max zero-guess prefix length (kernel
+        # register prefetch depth, csrc/amg.cu launch_sweep)
+        cw = np.zeros(2 * max(split.ncolors, 1), dtype=np.int32)
+        ll, lo = h.lane_len, h.lane_len_lo
+        for k in range(split.ncolors):
+            a, e = int(slices[k]) * 32, int(slices[k + 1]) * 32
+            if e > a:
+                cw[2 * k] = int(ll[a:e].max())
+                cw[2 * k + 1] = int(lo[a:e].max())
+        self.color_width = cw
+        self.desc.color_width = N.p32(self.color_width)
         self.desc.smoother = self.sell.desc
         self.desc.diag = D.ptr(self.diag)
         self.desc.b = D.ptr(self.b)

@@ -151,7 +151,7 @@ def test_bilu_apply_bitwise_given_factors(gpu, wave):
                                          int(rng.integers(2, 7)))) for _ in range(6)]
     cases += [_csr(random_sparse(rng, int(rng.integers(3, 300)), 6)),
               _bsr(random_block(rng, 1, 3, 1)), _bsr(random_block(rng, 700, 3, 12))]
-    for M in cases:
+    for ci, M in enumerate(cases):
         F = P.bilu0_factorize(M)
         Fo = _oracle_bilu(F)
         r = rng.standard_normal(Fo.n * Fo.b)
@@ -160,7 +160,7 @@ def test_bilu_apply_bitwise_given_factors(gpu, wave):
         z = torch.empty_like(rd)
         for _ in range(2):                                   # re-armed tickets / sentinels
             dev.apply(rd, z)
-            assert np.array_equal(z.cpu().numpy(), orc.bilu_apply(Fo, r))
+            assert np.array_equal(z.cpu().numpy(), orc.bilu_apply(Fo, r)), ci
 
 
 def test_bilu_apply_c1_vs_reference(gpu):

@@ -38,6 +38,8 @@ def main():
         "spmv": lambda: P.spmv(A, bd),
         "bilu": lambda: Bd.bilu.apply(bd, z),
         "vcycle": lambda: Bd.amg.vcycle(bd, zp),
+        "vcycleg": lambda: N.check(N.lib().cprb_amg_cycle_graph(Bd.graphs, C.byref(Bd.amg.desc),
+                                                                D.ptr(bd), D.ptr(zp), D.stream())),
         "solve": lambda: P.gmres_solve(A, bd, None, B, cfg.gmres_params()),
     }
     import ctypes as C
@@ -59,6 +61,34 @@ def main():
         print("tail phases", len(d), "total us", (L[-1] - L[0]) / 1e3)
         print(" ".join(f"{v:.2f}" for v in d))
         return
+    if a.what == "amgtl":
+        t = torch
+        log = t.zeros(4 * 4096, dtype=t.int64, device="cuda")
+        for rep in range(4):
+            log.zero_()
+            N.lib().cprb_amg_set_log(D.ptr(log))
+            if a.nograph:
+                Bd.amg.vcycle(bd, zp)
+            else:
+                N.check(N.lib().cprb_amg_cycle_graph(Bd.graphs, C.byref(Bd.amg.desc), D.ptr(bd),
+                                                     D.ptr(zp), D.stream()))
+            t.cuda.synchronize()
+        N.lib().cprb_amg_set_log(None)
+        L = log.cpu().numpy().reshape(-1, 4)
+        L = L[L[:, 1] > 0]
+        L = L[np.argsort(L[:, 1])]
+        t0 = L[0, 1]
+        names = {1: "sweep", 2: "sweepZG", 3: "rr", 4: "prol"}
+        tot = (L[-1, 3] - t0) / 1e3
+        print("launches", len(L), "span us", tot)
+        gaps = (L[1:, 1] - L[:-1, 3]) / 1e3
+        waits = (L[:, 2] - L[:, 1]) / 1e3
+        work = (L[:, 3] - L[:, 2]) / 1e3
+        print("median: start-gap(prev end->start)", np.median(gaps), "wait", np.median(waits), "work", np.median(work))
+        for i in range(0, len(L)):
+            if i < 60 or i % 20 == 0:
+                print(f"{i:4d} {names.get(int(L[i,0]),'?'):8s} start {(L[i,1]-t0)/1e3:8.2f} wait {(L[i,2]-L[i,1])/1e3:6.2f} work {(L[i,3]-L[i,2])/1e3:6.2f}")
+        return
     if a.what == "wavetl":
         t = torch
         log = t.zeros(2 * 256 * 512, dtype=t.int64, device="cuda")
@@ -71,7 +101,7 @@ def main():
         L = log.cpu().numpy().reshape(2, 256, 512)
         t0 = L[L > 0].min()
         for u in range(2):
-            nch = int((L[u, :, 0] > 0).sum())
+            nch = int((L[u, :200, 0] > 0).sum())
             print(("U" if u else "L"), "chunks", nch)
             for c in list(range(min(nch, 4))) + [nch // 2, nch - 1]:
                 row = L[u, c]
@@ -79,6 +109,10 @@ def main():
                 d = np.diff(row)
                 print(f" chunk {c}: start {(row[0]-t0)/1e3:.1f} end {(row[-1]-t0)/1e3:.1f} us, steps {row.size},"
                       f" median step {np.median(d)/1e3:.3f} us, max step {d.max()/1e3:.2f}")
+            F = L[u, 200:205, :128].astype(np.float64) / 280.0   # chunk 0 (c % 4 == 0 slot), cycles/step
+            nm = ["wait_full", "prefetch_next", "row(loads+spin+fp)", "publish+stores", "syncwarp+arrive"]
+            print("  cycles/step tid0:", {nm[q]: round(F[q, 0]) for q in range(5)})
+            print("  cycles/step mean over threads:", {nm[q]: round(F[q].mean()) for q in range(5)})
             # lag between consecutive chunks at equal local step 100
             lag = [(L[u, c, 100] - L[u, c - 1, 100]) / 1e3 for c in range(1, nch) if L[u, c, 100] > 0]
             print(" lag@step100 median", np.median(lag), "first", lag[:5])
