@@ -185,6 +185,8 @@ extern "C" int cprb_bilu_apply(const cprb_bilu* F, const double* r, double* z, d
   int rc = fill_sentinel(work_l, n, st);
   if (rc) return rc;
   if (F->use_wave) {
+    rc = fill_sentinel(z, n, st);  // the U solve polls its own output
+    if (rc) return rc;
     rc = wave_scatter_rhs(*F, r, F->rhs_l, st);
     if (rc) return rc;
     return wave_solve(*F, F->rhs_l, work_l, F->rhs_u, z, nullptr, nullptr, st);

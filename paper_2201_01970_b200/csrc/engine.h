@@ -32,7 +32,8 @@ int set_error(int code, const std::string& msg);
 int check_launch(const char* what);
 
 int bsr_op(int mode, const cprb_sell& A, int b, const double* x, const double* rhs, double* out,
-           int32_t* flag, double* sent, cudaStream_t st, const int32_t* out_idx = nullptr);
+           int32_t* flag, double* sent, cudaStream_t st, const int32_t* out_idx = nullptr,
+           double* sent2 = nullptr);
 int wave_solve(const cprb_bilu& F, const double* rhsL, double* zl, double* zu_rhs, double* y,
                const double* zp, double* zout, cudaStream_t st);
 int wave_scatter_rhs(const cprb_bilu& F, const double* r, double* rhsL, cudaStream_t st);

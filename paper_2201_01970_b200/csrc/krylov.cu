@@ -228,7 +228,8 @@ int cprb_cpr_finish(const cprb_cpr* P, const double* r, double* z, void* stream)
   const cprb_bilu& F = P->bilu;
   if (F.use_wave) {
     // stage-2 residual written straight into the L plan's step order
-    int rc = bsr_op(2, P->A, P->b, P->zp, r, F.rhs_l, nullptr, P->zl, st, F.l_slot);
+    // (also arms zl and y, the sentinel-polled outputs of the L and U solves)
+    int rc = bsr_op(2, P->A, P->b, P->zp, r, F.rhs_l, nullptr, P->zl, st, F.l_slot, P->y);
     if (rc) return rc;
     return wave_solve(F, F.rhs_l, P->zl, F.rhs_u, P->y, P->zp, z, st);
   }

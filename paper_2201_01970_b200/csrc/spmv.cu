@@ -66,7 +66,7 @@ template <int B, int MODE>
 __global__ void __launch_bounds__(BSR_WARPS * 32, 4)
     k_bsr(const cprb_sell A, const double* __restrict__ x, const double* __restrict__ rhs,
           double* __restrict__ out, int32_t* flag, double* __restrict__ sent,
-          const int32_t* __restrict__ out_idx) {
+          double* __restrict__ sent2, const int32_t* __restrict__ out_idx) {
   pdl_trigger();
   const int gw = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
@@ -98,29 +98,31 @@ __global__ void __launch_bounds__(BSR_WARPS * 32, 4)
   const int64_t ob = out_idx ? (int64_t)out_idx[row] + r : o;
   out[ob] = v;
   if (MODE == 2 && sent) sent[o] = sentinel();
+  if (MODE == 2 && sent2) sent2[o] = sentinel();
   flag_nonfinite(flag, !isfinite(v));
 }
 
 template <int B, int MODE>
 static void launch_bsr(const cprb_sell& A, const double* x, const double* rhs, double* out,
-                       int32_t* flag, double* sent, cudaStream_t st, const int32_t* oi) {
+                       int32_t* flag, double* sent, double* sent2, cudaStream_t st,
+                       const int32_t* oi) {
   if (A.nslices <= 0) return;
   const int threads = BSR_WARPS * 32;
   const int64_t warps = (int64_t)A.nslices * B;
   const int blocks = (int)((warps + BSR_WARPS - 1) / BSR_WARPS);
-  launch_pdl(k_bsr<B, MODE>, blocks, threads, 0, st, A, x, rhs, out, flag, sent, oi);
+  launch_pdl(k_bsr<B, MODE>, blocks, threads, 0, st, A, x, rhs, out, flag, sent, sent2, oi);
 }
 
 int bsr_op(int mode, const cprb_sell& A, int b, const double* x, const double* rhs, double* out,
-           int32_t* flag, double* sent, cudaStream_t st, const int32_t* oi) {
+           int32_t* flag, double* sent, cudaStream_t st, const int32_t* oi, double* sent2) {
   if (b == 3) {
-    if (mode == 0) launch_bsr<3, 0>(A, x, rhs, out, flag, sent, st, oi);
-    else if (mode == 1) launch_bsr<3, 1>(A, x, rhs, out, flag, sent, st, oi);
-    else launch_bsr<3, 2>(A, x, rhs, out, flag, sent, st, oi);
+    if (mode == 0) launch_bsr<3, 0>(A, x, rhs, out, flag, sent, sent2, st, oi);
+    else if (mode == 1) launch_bsr<3, 1>(A, x, rhs, out, flag, sent, sent2, st, oi);
+    else launch_bsr<3, 2>(A, x, rhs, out, flag, sent, sent2, st, oi);
   } else if (b == 1) {
-    if (mode == 0) launch_bsr<1, 0>(A, x, rhs, out, flag, sent, st, oi);
-    else if (mode == 1) launch_bsr<1, 1>(A, x, rhs, out, flag, sent, st, oi);
-    else launch_bsr<1, 2>(A, x, rhs, out, flag, sent, st, oi);
+    if (mode == 0) launch_bsr<1, 0>(A, x, rhs, out, flag, sent, sent2, st, oi);
+    else if (mode == 1) launch_bsr<1, 1>(A, x, rhs, out, flag, sent, sent2, st, oi);
+    else launch_bsr<1, 2>(A, x, rhs, out, flag, sent, sent2, st, oi);
   } else {
     return set_error(CPRB_EUNSUPPORTED, "block size " + std::to_string(b) + " not supported on device");
   }

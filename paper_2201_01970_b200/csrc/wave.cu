@@ -31,6 +31,10 @@ constexpr int WAVE_DINT = 3;       // == ilu.WAVE_DINT: ring-served dependency d
 constexpr int WAVE_RING = 8;       // result ring; >= DEPTH + DINT (no overwrite while read)
 constexpr int WAVE_KPRE = 3;       // external dependencies prefetched per row
 constexpr int WAVE_META = 1024;    // step metadata staged in shared memory per chunk
+// lens[] word: low 16 bits = dependency count; bit 30 = the row's value must be
+// published to global memory (another chunk or an older-than-DINT row reads it)
+constexpr int WAVE_LEN_MASK = 0xFFFF;
+constexpr int WAVE_EXPORT = 1 << 30;
 static_assert(WAVE_RING >= WAVE_DEPTH + WAVE_DINT, "result ring too small");
 
 // diagnostic timeline (cprb_wave_set_log): [UPPER][chunk][local step] ->
@@ -317,8 +321,9 @@ __device__ __forceinline__ void lean_row(uint32_t sblk, uint32_t srhs, uint32_t 
   }
 }
 
-// UPPER = false: z = r - sum L z   (publishes z, copies z into the U plan's
-//                rhs order via aux slots, arms y with the sentinel)
+// UPPER = false: z = r - sum L z   (publishes exported z rows, copies z into
+//                the U plan's rhs order via aux slots; y must be armed with
+//                the sentinel by the caller)
 // UPPER = true : y = Uinv (z - sum U y); final = z1 + y
 template <int B, bool UPPER>
 __global__ void __launch_bounds__(WAVE_BLOCK, 1)
@@ -395,7 +400,13 @@ __global__ void __launch_bounds__(WAVE_BLOCK, 1)
         for (int k = s0; k < s1; ++k) {
           const uint32_t gg = g + (uint32_t)(k - s0);
           const int st = gg % WAVE_DEPTH;
+          const long long t_pw = clock64();
           if (gg >= WAVE_DEPTH) mbar_wait(&S.empty[st], ((gg / WAVE_DEPTH) - 1) & 1);
+          if (g_wave_log && c == 0 && k - s0 < WAVE_LOG_STEPS) {
+            const long long t_is = clock64();
+            g_wave_log[((UPPER ? 1 : 0) * WAVE_LOG_CHUNKS + 206) * WAVE_LOG_STEPS + (k - s0)] = (unsigned long long)t_is;
+            g_wave_log[((UPPER ? 1 : 0) * WAVE_LOG_CHUNKS + 208) * WAVE_LOG_STEPS + (k - s0)] = (unsigned long long)(t_is - t_pw);
+          }
           const StepMeta m = meta(k);
           mbar_expect_tx(&S.full[st], (uint32_t)(m.bytes + m.rhs_bytes));
           bulk_g2s(S.stage + (size_t)st * stage_max, W.stream + m.off, m.bytes, &S.full[st]);
@@ -405,6 +416,7 @@ __global__ void __launch_bounds__(WAVE_BLOCK, 1)
       }
       __syncwarp();
     } else {
+      const int pos = tid;  // row position of every step handled by this thread
       long long cyc[5] = {0, 0, 0, 0, 0};
       long long tlast = clock64();
       Pre<B> pre;
@@ -414,7 +426,7 @@ __global__ void __launch_bounds__(WAVE_BLOCK, 1)
         const int w = meta(s0).w;
         const int Wp = (w + 3) & ~3;
         const int32_t* rows = reinterpret_cast<const int32_t*>(S.stage + (size_t)st * stage_max);
-        if (tid < w) wave_prefetch<B>(rows + 3 * Wp, Wp, tid, rows[Wp + tid], out_nat, pre);
+        if (pos < w) wave_prefetch<B>(rows + 3 * Wp, Wp, pos, rows[Wp + pos] & WAVE_LEN_MASK, out_nat, pre);
       }
       for (int k = s0; k < s1; ++k) {
         const uint32_t gk = g + (uint32_t)(k - s0);
@@ -429,6 +441,8 @@ __global__ void __launch_bounds__(WAVE_BLOCK, 1)
         };
         tmark(0);
         mbar_wait(&S.full[st], (gk / WAVE_DEPTH) & 1);
+        if (tid == 0 && g_wave_log && c == 0 && k - s0 < WAVE_LOG_STEPS)
+          g_wave_log[((UPPER ? 1 : 0) * WAVE_LOG_CHUNKS + 207) * WAVE_LOG_STEPS + (k - s0)] = (unsigned long long)clock64();
         tmark(1);
         const uint8_t* blk = S.stage + (size_t)st * stage_max;
         const StepMeta mk = meta(k);
@@ -441,48 +455,38 @@ __global__ void __launch_bounds__(WAVE_BLOCK, 1)
         const double* vals = reinterpret_cast<const double*>(blk + (size_t)(12 + 4 * K) * Wp);
         const double* uinv = vals + (size_t)K * BB * Wp;
         const double* rhs = S.rhs + (size_t)st * (rhs_max / 8);
-        // issue the next step's cross-chunk dependency loads now (if its
-        // record has landed), so their L2 round trip overlaps this step
         Pre<B> nxt;
-        if (k + 1 < s1) {
-          const uint32_t g1 = gk + 1;
-          const int st1 = g1 % WAVE_DEPTH;
-          mbar_wait(&S.full[st1], (g1 / WAVE_DEPTH) & 1);
-          const int w1 = meta(k + 1).w;
-          const int Wp1 = (w1 + 3) & ~3;
-          const int32_t* r1 = reinterpret_cast<const int32_t*>(S.stage + (size_t)st1 * stage_max);
-          if (tid < w1) wave_prefetch<B>(r1 + 3 * Wp1, Wp1, tid, r1[Wp1 + tid], out_nat, nxt);
-        }
         tmark(2);
-        if (tid < w && K <= WAVE_KPRE) {
+        if (pos < w && K <= WAVE_KPRE) {
           // lean path (all rows of 7-point-type factors)
           const uint32_t sblk = smem_u32(blk);
           const uint32_t srhs = smem_u32(rhs);
-          const int row = lds_s32(sblk + 4u * tid);
-          const int len = lds_s32(sblk + 4u * (Wp + tid));
-          const int ns = UPPER ? 0 : lds_s32(sblk + 4u * (2 * Wp + tid));
+          const int row = lds_s32(sblk + 4u * pos);
+          const int lenw = lds_s32(sblk + 4u * (Wp + pos));
+          const int len = lenw & WAVE_LEN_MASK;
+          const bool publish = (lenw & WAVE_EXPORT) || (UPPER && !final_out);
+          const int ns = UPPER ? 0 : lds_s32(sblk + 4u * (2 * Wp + pos));
           double z1 = 0.0;
           if (UPPER && zp) z1 = zp[row];
           double res[B];
           switch (K) {
-            case 0: lean_row<B, UPPER, 0>(sblk, srhs, sring, sflag, Wp, tid, k, len, out_nat, pre, res); break;
-            case 1: lean_row<B, UPPER, 1>(sblk, srhs, sring, sflag, Wp, tid, k, len, out_nat, pre, res); break;
-            case 2: lean_row<B, UPPER, 2>(sblk, srhs, sring, sflag, Wp, tid, k, len, out_nat, pre, res); break;
-            default: lean_row<B, UPPER, 3>(sblk, srhs, sring, sflag, Wp, tid, k, len, out_nat, pre, res); break;
+            case 0: lean_row<B, UPPER, 0>(sblk, srhs, sring, sflag, Wp, pos, k, len, out_nat, pre, res); break;
+            case 1: lean_row<B, UPPER, 1>(sblk, srhs, sring, sflag, Wp, pos, k, len, out_nat, pre, res); break;
+            case 2: lean_row<B, UPPER, 2>(sblk, srhs, sring, sflag, Wp, pos, k, len, out_nat, pre, res); break;
+            default: lean_row<B, UPPER, 3>(sblk, srhs, sring, sflag, Wp, pos, k, len, out_nat, pre, res); break;
           }
           tmark(3);
-          const uint32_t slot = (uint32_t)((k % WAVE_RING) * WAVE_THREADS + tid);
+          const uint32_t slot = (uint32_t)((k % WAVE_RING) * WAVE_THREADS + pos);
 #pragma unroll
           for (int r = 0; r < B; ++r) sts_f64(sring + 8u * (slot * B + r), res[r]);
           sts_release_s32(sflag + 4u * slot, k);
+          if (publish) {
 #pragma unroll
-          for (int r = 0; r < B; ++r) st_relaxed(out_nat + (int64_t)B * row + r, res[r]);
+            for (int r = 0; r < B; ++r) st_relaxed(out_nat + (int64_t)B * row + r, res[r]);
+          }
           if constexpr (!UPPER) {
 #pragma unroll
-            for (int r = 0; r < B; ++r) {
-              next_rhs[(int64_t)ns + r] = res[r];
-              arm[(int64_t)B * row + r] = sentinel();
-            }
+            for (int r = 0; r < B; ++r) next_rhs[(int64_t)ns + r] = res[r];
           } else {
             if (final_out) {
 #pragma unroll
@@ -490,11 +494,13 @@ __global__ void __launch_bounds__(WAVE_BLOCK, 1)
                 final_out[(int64_t)B * row + r] = zp ? ((r == 0 ? z1 : 0.0) + res[r]) : res[r];
             }
           }
-        } else if (tid < w) {
+        } else if (pos < w) {
           RingRef ring = ring0;
           ring.k = k;
-          const int row = rows[tid];
-          const int len = lens[tid];
+          const int row = rows[pos];
+          const int lenw = lens[pos];
+          const int len = lenw & WAVE_LEN_MASK;
+          const bool publish = (lenw & WAVE_EXPORT) || (UPPER && !final_out);
           double z1 = 0.0;
           if (UPPER && zp) z1 = zp[row];
           double ts[B];
@@ -503,39 +509,38 @@ __global__ void __launch_bounds__(WAVE_BLOCK, 1)
 #pragma unroll
               for (int r = 0; r < B; ++r) ts[r] = 0.0;
               break;
-            case 1: wave_rowsum_fixed<B, 1>(codes, vals, Wp, tid, ring, out_nat, pre, ts); break;
-            case 2: wave_rowsum_fixed<B, 2>(codes, vals, Wp, tid, ring, out_nat, pre, ts); break;
-            case 3: wave_rowsum_fixed<B, 3>(codes, vals, Wp, tid, ring, out_nat, pre, ts); break;
-            default: wave_rowsum_generic<B>(codes, vals, Wp, tid, len, ring, out_nat, pre, ts); break;
+            case 1: wave_rowsum_fixed<B, 1>(codes, vals, Wp, pos, ring, out_nat, pre, ts); break;
+            case 2: wave_rowsum_fixed<B, 2>(codes, vals, Wp, pos, ring, out_nat, pre, ts); break;
+            case 3: wave_rowsum_fixed<B, 3>(codes, vals, Wp, pos, ring, out_nat, pre, ts); break;
+            default: wave_rowsum_generic<B>(codes, vals, Wp, pos, len, ring, out_nat, pre, ts); break;
           }
           double res[B];
           if constexpr (!UPPER) {
 #pragma unroll
-            for (int r = 0; r < B; ++r) res[r] = rhs[tid * B + r] - ts[r];
+            for (int r = 0; r < B; ++r) res[r] = rhs[pos * B + r] - ts[r];
           } else {
             double d[B], ui[BB];
 #pragma unroll
-            for (int r = 0; r < B; ++r) d[r] = rhs[tid * B + r] - ts[r];
+            for (int r = 0; r < B; ++r) d[r] = rhs[pos * B + r] - ts[r];
 #pragma unroll
-            for (int e = 0; e < BB; ++e) ui[e] = uinv[(size_t)e * Wp + tid];
+            for (int e = 0; e < BB; ++e) ui[e] = uinv[(size_t)e * Wp + pos];
 #pragma unroll
             for (int r = 0; r < B; ++r) res[r] = block_row_dot<B>(&ui[r * B], d);
           }
           tmark(3);
-          const int slot = (k % WAVE_RING) * WAVE_THREADS + tid;
+          const int slot = (k % WAVE_RING) * WAVE_THREADS + pos;
           double* ring_slot = S.ring + (size_t)slot * B;
 #pragma unroll
           for (int r = 0; r < B; ++r) ring_slot[r] = res[r];
           st_release_s32(S.flag + slot, k);
+          if (publish) {
 #pragma unroll
-          for (int r = 0; r < B; ++r) st_relaxed(out_nat + (int64_t)B * row + r, res[r]);
+            for (int r = 0; r < B; ++r) st_relaxed(out_nat + (int64_t)B * row + r, res[r]);
+          }
           if constexpr (!UPPER) {
-            const int ns = aux[tid];
+            const int ns = aux[pos];
 #pragma unroll
-            for (int r = 0; r < B; ++r) {
-              next_rhs[(int64_t)ns + r] = res[r];
-              arm[(int64_t)B * row + r] = sentinel();
-            }
+            for (int r = 0; r < B; ++r) next_rhs[(int64_t)ns + r] = res[r];
           } else {
             if (final_out) {
 #pragma unroll
@@ -549,6 +554,18 @@ __global__ void __launch_bounds__(WAVE_BLOCK, 1)
           asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tt));
           g_wave_log[((UPPER ? 1 : 0) * WAVE_LOG_CHUNKS + c) * WAVE_LOG_STEPS + (k - s0)] = tt;
         }
+        // after this step's row is published: issue the next step's
+        // cross-chunk dependency loads (if its record has landed), so their
+        // L2 round trip overlaps the global stores and the step hand-off
+        if (k + 1 < s1) {
+          const uint32_t g1 = gk + 1;
+          const int st1 = g1 % WAVE_DEPTH;
+          mbar_wait(&S.full[st1], (g1 / WAVE_DEPTH) & 1);
+          const int w1 = meta(k + 1).w;
+          const int Wp1 = (w1 + 3) & ~3;
+          const int32_t* r1 = reinterpret_cast<const int32_t*>(S.stage + (size_t)st1 * stage_max);
+          if (pos < w1) wave_prefetch<B>(r1 + 3 * Wp1, Wp1, pos, r1[Wp1 + pos] & WAVE_LEN_MASK, out_nat, nxt);
+        }
         tmark(4);
         __syncwarp();
         if ((tid & 31) == 0) mbar_arrive(&S.empty[st]);  // this warp is done with the slot
@@ -556,7 +573,7 @@ __global__ void __launch_bounds__(WAVE_BLOCK, 1)
         tmark(5);
       }
       if (g_wave_log && c < WAVE_LOG_CHUNKS && tid < 128) {
-        // cycles per phase summed over the chunk, slot [UPPER][200 + phase][chunk*... ] tid-major
+        // cycles per phase summed over the chunk, slot [UPPER][200 + phase][chunk*... ] pos-major
         for (int q = 0; q < 5; ++q)
           g_wave_log[((UPPER ? 1 : 0) * WAVE_LOG_CHUNKS + 200 + q) * WAVE_LOG_STEPS + (c % 4) * 128 + tid] =
               (unsigned long long)cyc[q];

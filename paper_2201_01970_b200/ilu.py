@@ -12,6 +12,8 @@ from __future__ import annotations
 import ctypes as C
 from dataclasses import dataclass, field
 
+import os
+
 import numpy as np
 
 from . import _native as N
@@ -151,10 +153,10 @@ def _level_sell(T: BlockCsrMatrix, sched: LevelSchedule, b: int, uinv=None):
     return h, ui
 
 
-WAVE_WMAX = 128         # rows per step == threads per CTA (csrc/wave.cu)
+WAVE_WMAX = 128         # rows per step == consumer threads per CTA (csrc/wave.cu)
 WAVE_DINT = 3           # dependencies at most this many steps back are read from shared memory
 WAVE_STAGE_CAP = 40960  # bytes per streamed step
-WAVE_BANDS = 2          # dependency bandwidths (xy-planes) per chunk
+WAVE_BANDS = int(os.environ.get("CPRB_WAVE_BANDS", "2"))  # dependency bandwidths (xy-planes) per chunk
 
 
 def _round16(x):
@@ -215,13 +217,19 @@ def wave_plan(T: BlockCsrMatrix, sched: LevelSchedule, b: int, upper: bool, uinv
         if nsteps < 4096 else (step_w * b * 8 + 15) // 16 * 16
     roff = np.zeros(nsteps + 1, dtype=np.int64)
     np.cumsum(rbytes // 8, out=roff[1:])
+    # rows some dependant polls from global memory (another chunk, or more
+    # than WAVE_DINT steps later): only these are published by the kernel
+    e_diff = row_step[rows_of] - row_step[cols]
+    e_int = (chunk[cols] == chunk[rows_of]) & (e_diff >= 1) & (e_diff <= WAVE_DINT)
+    exported = np.zeros(n, dtype=bool)
+    exported[cols[~e_int]] = True
     stream = np.zeros(max(int(soff[-1]), 16), dtype=np.uint8)
     I = stream.view(np.int32)
     F = stream.view(np.float64)
     st = row_step
     base4 = soff[st] // 4
     I[base4 + row_pos] = np.arange(n)                              # rows
-    I[base4 + Wp[st] + row_pos] = lens                              # lens
+    I[base4 + Wp[st] + row_pos] = lens | (exported.astype(np.int64) << 30)  # lens | export bit
     aux = np.zeros(n, dtype=np.int64) if aux_slot is None else aux_slot
     I[base4 + 2 * Wp[st] + row_pos] = aux                           # aux (next rhs slot)
     # entries

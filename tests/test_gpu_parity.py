@@ -199,6 +199,27 @@ def test_vcycle_matches_oracle_with_same_coarse_solve(gpu):
     np.testing.assert_allclose(P.amg_cycle(B.pressure_solver, r), zo, rtol=1e-13, atol=1e-15)
 
 
+@pytest.mark.parametrize("tail_rows", ["100000000", "300"])
+def test_vcycle_persistent_tail_bitwise(gpu, monkeypatch, tail_rows):
+    """The cluster-resident V-cycle tail (csrc/amg.cu k_vtail) runs the same
+    arithmetic as the per-colour kernels: bitwise equal cycles, whole cycle
+    in the tail (C1) or only the coarse levels."""
+    A, _ = _c1()
+    (A2, _), = P.generate_blackoil_like_sequence(16, 12, 10, 1, 0.01, 1).systems
+    rng = np.random.default_rng(11)
+    for M in (A, A2):
+        cfg = P.SolverConfig(theta=0.0, theta_amg=0.0, cycle="v")
+        h0 = P.build_hierarchy(P.pressure_matrix(M), cfg.amg_params())
+        r = rng.standard_normal(M.nrows)
+        z0 = P.amg_cycle(h0, r)
+        monkeypatch.setenv("CPRB_TAIL_ROWS", tail_rows)
+        h1 = P.build_hierarchy(P.pressure_matrix(M), cfg.amg_params())
+        z1 = P.amg_cycle(h1, r)
+        assert h1.device().desc.tail_start < len(h1.levels) - 1
+        monkeypatch.delenv("CPRB_TAIL_ROWS")
+        assert np.array_equal(z0, z1)
+
+
 def test_cpr_product_form_identity(gpu):
     """Eq. 8 (tests/test_cpr.py:98-118): I - B A = (I - R A)(I - Pi B_P Pi^T A)."""
     rng = np.random.default_rng(20240817)

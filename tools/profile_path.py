@@ -111,6 +111,14 @@ def main():
                       f" median step {np.median(d)/1e3:.3f} us, max step {d.max()/1e3:.2f}")
             F = L[u, 200:205, :128].astype(np.float64) / 280.0   # chunk 0 (c % 4 == 0 slot), cycles/step
             nm = ["wait_full", "prefetch_next", "row(loads+spin+fp)", "publish+stores", "syncwarp+arrive"]
+            iss = L[u, 206, :279].astype(np.float64)
+            got = L[u, 207, :279].astype(np.float64)
+            pw = L[u, 208, :279].astype(np.float64)
+            if iss[5] > 0:
+                lat = got - iss
+                print("  TMA issue->landed-seen (cycles) median", np.median(lat[4:]), "p90", np.percentile(lat[4:], 90),
+                      "| producer wait on empty median", np.median(pw[4:]),
+                      "| issue interval median", np.median(np.diff(iss[4:])))
             print("  cycles/step tid0:", {nm[q]: round(F[q, 0]) for q in range(5)})
             print("  cycles/step mean over threads:", {nm[q]: round(F[q].mean()) for q in range(5)})
             # lag between consecutive chunks at equal local step 100
