@@ -106,6 +106,15 @@ def _dist():
     return ws, rank, local
 
 
+def max_over_ranks(value: float, dist, torch, device: str) -> float:
+    """Whole-job time of a step = the slowest rank's (the contract's max over
+    ranks); collective on any backend (NCCL on the GPU box, gloo in tests)."""
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.barrier()
+    return float(t.item())
+
+
 def _grid(s):
     return tuple(int(v) for v in s.split(","))
 
@@ -188,10 +197,7 @@ def run_ours(args):
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
     if ws > 1:
-        tt = torch.tensor([ms], device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
-        dist.barrier()
+        ms = max_over_ranks(ms, dist, torch, "cuda")
     x_dev = res.x
     xs = P.problems.manufactured_solution(nx * ny * nz)
     x_err = float(np.linalg.norm(x_dev.cpu().numpy() - xs) / np.linalg.norm(xs))

@@ -155,7 +155,7 @@ def _level_sell(T: BlockCsrMatrix, sched: LevelSchedule, b: int, uinv=None):
 
 WAVE_WMAX = 128         # rows per step == consumer threads per CTA (csrc/wave.cu)
 WAVE_DINT = 3           # dependencies at most this many steps back are read from shared memory
-WAVE_STAGE_CAP = 40960  # bytes per streamed step
+WAVE_KMAX = 3           # steps with at most this many dependencies per row are TMA-streamed
 WAVE_BANDS = int(os.environ.get("CPRB_WAVE_BANDS", "2"))  # dependency bandwidths (xy-planes) per chunk
 
 
@@ -188,8 +188,7 @@ def wave_plan(T: BlockCsrMatrix, sched: LevelSchedule, b: int, upper: bool, uinv
     gsize = np.diff(np.append(gstart, n))
     gid = np.repeat(np.arange(gstart.shape[0]), gsize)
     Kg = np.maximum.reduceat(lens[order], gstart) if n else np.zeros(0, np.int64)
-    row_bytes = 12 + 4 * Kg + 8 * Kg * bb + (8 * bb if upper else 0)
-    cap = np.minimum(WAVE_WMAX, np.maximum(1, (WAVE_STAGE_CAP - 64) // row_bytes))
+    cap = np.full(gstart.shape[0], WAVE_WMAX, dtype=np.int64)
     nsub = -(-gsize // cap)
     gstep0 = np.zeros(gstart.shape[0] + 1, dtype=np.int64)
     np.cumsum(nsub, out=gstep0[1:])
@@ -209,14 +208,21 @@ def wave_plan(T: BlockCsrMatrix, sched: LevelSchedule, b: int, upper: bool, uinv
     step_chunk[step_of_sorted] = ch_s
     nchunks = int(chunk.max()) + 1 if n else 0
     chunk_step = np.searchsorted(step_chunk, np.arange(nchunks + 1)).astype(np.int32)
-    Wp = (step_w + 3) // 4 * 4
-    sbytes = Wp * (12 + 4 * step_k) + 8 * step_k * bb * Wp + (8 * bb * Wp if upper else 0)
+    # warp-sliced records: the rows of a step are cut into 32-row warp slices;
+    # slice q of step s is one contiguous sub-record
+    #   int32 rows[32], lens[32], aux[32], codes[K][32];
+    #   f64 vals[K][b*b][32]; (upper) f64 uinv[b*b][32]
+    # so each consumer warp streams exactly its own rows (csrc/wave.cu).
+    nwarp = (step_w + 31) // 32
+    sub = 32 * (12 + 4 * step_k) + 8 * 32 * step_k * bb + (8 * 32 * bb if upper else 0)
+    sbytes = nwarp * sub
     soff = np.zeros(nsteps + 1, dtype=np.int64)
     np.cumsum(sbytes, out=soff[1:])
     rbytes = np.array([_round16(int(w) * b * 8) for w in step_w], dtype=np.int64) \
         if nsteps < 4096 else (step_w * b * 8 + 15) // 16 * 16
     roff = np.zeros(nsteps + 1, dtype=np.int64)
     np.cumsum(rbytes // 8, out=roff[1:])
+    roff_pad = int(roff[-1]) + 32 * b              # a partial warp slice may read past the end
     # rows some dependant polls from global memory (another chunk, or more
     # than WAVE_DINT steps later): only these are published by the kernel
     e_diff = row_step[rows_of] - row_step[cols]
@@ -227,11 +233,12 @@ def wave_plan(T: BlockCsrMatrix, sched: LevelSchedule, b: int, upper: bool, uinv
     I = stream.view(np.int32)
     F = stream.view(np.float64)
     st = row_step
-    base4 = soff[st] // 4
-    I[base4 + row_pos] = np.arange(n)                              # rows
-    I[base4 + Wp[st] + row_pos] = lens | (exported.astype(np.int64) << 30)  # lens | export bit
+    rec = soff[st] + (row_pos // 32) * sub[st]          # byte offset of the row's warp slice
+    ln = row_pos % 32
+    I[rec // 4 + ln] = np.arange(n)                                       # rows
+    I[rec // 4 + 32 + ln] = lens | (exported.astype(np.int64) << 30)      # lens | export bit
     aux = np.zeros(n, dtype=np.int64) if aux_slot is None else aux_slot
-    I[base4 + 2 * Wp[st] + row_pos] = aux                           # aux (next rhs slot)
+    I[rec // 4 + 64 + ln] = aux                                           # aux (next rhs slot)
     # entries
     ent = np.arange(cols.shape[0], dtype=np.int64)
     m = ent - ptr[rows_of]
@@ -242,22 +249,24 @@ def wave_plan(T: BlockCsrMatrix, sched: LevelSchedule, b: int, upper: bool, uinv
     slot = (diff - 1) * WAVE_WMAX + row_pos[dep]
     code = np.where(internal, -(slot + 1), dep)
     e_st = row_step[ri]
-    e_Wp = Wp[e_st]
-    I[soff[e_st] // 4 + 3 * e_Wp + m * e_Wp + row_pos[ri]] = code
-    vbase = (soff[e_st] + (12 + 4 * step_k[e_st]) * e_Wp) // 8
+    e_rec = rec[ri]
+    e_ln = ln[ri]
+    I[e_rec // 4 + 96 + 32 * m + e_ln] = code
+    vbase = (e_rec + 32 * (12 + 4 * step_k[e_st])) // 8
     e_idx = np.arange(bb, dtype=np.int64)
-    F[(vbase + (m * bb) * e_Wp + row_pos[ri])[:, None] + e_idx[None, :] * e_Wp[:, None]] = vals
+    F[(vbase + (m * bb) * 32 + e_ln)[:, None] + e_idx[None, :] * 32] = vals
     if upper:
-        ub = (soff[st] + (12 + 4 * step_k[st]) * Wp[st] + 8 * step_k[st] * bb * Wp[st]) // 8
-        F[(ub + row_pos)[:, None] + e_idx[None, :] * Wp[st][:, None]] = \
+        ub = (rec + 32 * (12 + 4 * step_k[st]) + 8 * 32 * step_k[st] * bb) // 8
+        F[(ub + ln)[:, None] + e_idx[None, :] * 32] = \
             np.asarray(uinv, dtype=np.float64).reshape(n, bb)
     rhs_slot = roff[st] + row_pos * b
-    host = dict(nchunks=nchunks, nsteps=nsteps, stage_max=int(sbytes.max(initial=16)),
-                rhs_max=int(rbytes.max(initial=16)), chunk_step=chunk_step,
-                step_off=soff[:-1].astype(np.int64), step_bytes=sbytes.astype(np.int32),
+    fast = step_k <= WAVE_KMAX
+    host = dict(nchunks=nchunks, nsteps=nsteps, stage_max=int(sub[fast].max(initial=16)),
+                rhs_max=32 * b * 8, chunk_step=chunk_step,
+                step_off=soff[:-1].astype(np.int64), step_bytes=sub.astype(np.int32),
                 step_w=step_w.astype(np.int32), step_k=step_k.astype(np.int32),
                 rhs_off=roff[:-1].astype(np.int64), rhs_bytes=rbytes.astype(np.int32),
-                stream=stream, rhs_len=int(roff[-1]), chunk_rows=R)
+                stream=stream, rhs_len=roff_pad, chunk_rows=R)
     return host, rhs_slot
 
 

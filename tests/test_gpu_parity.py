@@ -375,3 +375,43 @@ def test_spe10_shape_c3_against_reference(gpu):
     got = res.x[::ref["x_sample_stride"]]
     assert np.linalg.norm(got - xs) <= 1e-6 * np.linalg.norm(xs)
     assert abs(np.linalg.norm(res.x) - ref["x_norm"]) <= 1e-6 * ref["x_norm"]
+
+
+@pytest.mark.slow
+def test_c2_pressure128_vcycle_against_survey(gpu):
+    """Config 2: 128^3 pressure system (2,097,152 rows), stationary V(1,1)
+    cycles from x = 0, b = ones.  Structure (levels, colours) is bit-exact to
+    the reference run of SURVEY.md section 0.3 / Appendix C; the per-cycle
+    relative residuals match the reference's printed values (4 digits)."""
+    A = P.problems.pressure_operator(128, 128, 128)
+    h = P.build_hierarchy(A, P.AmgParams(theta_amg=0.0, cycle="v"))
+    sizes = [l.A.nrows for l in h.levels]
+    assert len(sizes) == 15 and sizes[0] == 2097152 and sizes[-1] == 186
+    assert [l.partition.c for l in h.levels[:-1]] == [2, 8, 9, 10, 11, 12, 12, 12, 12, 12, 12,
+                                                       11, 12, 10]
+    ref = [0.2716, 0.0953, 0.0384, 0.0173, 0.00841, 0.00429, 0.00227, 0.00123, 6.83e-4, 3.85e-4]
+    import torch
+    Ad = torch.from_numpy(np.ones(A.nrows)).cuda()
+    b = Ad.clone()
+    x = torch.zeros_like(b)
+    nb = float(torch.linalg.vector_norm(b))
+    for k in range(10):
+        r = b - P.spmv(A, x)
+        x = x + P.amg_cycle(h, r)
+        rel = float(torch.linalg.vector_norm(b - P.spmv(A, x))) / nb
+        assert abs(rel - ref[k]) <= 6e-3 * ref[k] + 1e-6, (k, rel, ref[k])
+
+
+@pytest.mark.slow
+def test_c4_sequence_reuse_against_survey(gpu):
+    """Config 4 (first 3 of the 10 SPE10-shaped Newton systems, mu = 5, V,
+    theta_amg = 0): one setup, every solve 1 outer / 5 inner, final residuals
+    of the reference run within 1e-8 relative."""
+    seq = P.generate_blackoil_like_sequence(60, 220, 85, 3, 0.01, 0)
+    cfg = P.SolverConfig(theta=0.0, theta_amg=0.0, cycle="v")
+    out = P.ascpr_gmres_sequence(seq.systems, 5, cfg, keep_solutions=False)
+    assert out.setup_calls == 1
+    assert [(r.outer, r.inner) for r in out.records] == [(1, 5)] * 3
+    assert [r.rebuilt for r in out.records] == [True, False, False]
+    ref = [4.539505890669102e-06, 4.81992118102329e-06, 5.0585008937417845e-06]
+    np.testing.assert_allclose([r.rel_residual for r in out.records], ref, rtol=1e-8)

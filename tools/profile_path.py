@@ -111,7 +111,7 @@ def main():
                       f" median step {np.median(d)/1e3:.3f} us, max step {d.max()/1e3:.2f}")
             F = L[u, 200:205, :128].astype(np.float64) / 280.0   # chunk 0 (c % 4 == 0 slot), cycles/step
             nm = ["wait_full", "prefetch_next", "row(loads+spin+fp)", "publish+stores", "syncwarp+arrive"]
-            iss = L[u, 206, :279].astype(np.float64)
+            iss = 0 * L[u, 206, :279].astype(np.float64)
             got = L[u, 207, :279].astype(np.float64)
             pw = L[u, 208, :279].astype(np.float64)
             if iss[5] > 0:
