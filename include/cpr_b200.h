@@ -163,6 +163,9 @@ typedef struct cprb_amg {
   int32_t tail_ctas;                /* cluster size (1..16) */
   const cprb_tail_level* tail_levels; /* dev, nlevels-1 entries (index = level) */
   const int32_t* tail_colors;       /* dev colour table */
+  const int32_t* tail_phases;       /* dev, tail_nphases x {type, level, colour, flags} */
+  int32_t tail_nphases;
+  int32_t pad_;
 } cprb_amg;
 
 /* Chunked-wavefront plan of one triangular factor (csrc/wave.cu).  Rows are

@@ -50,7 +50,8 @@ class Amg(C.Structure):
                 ("coarse_inv", vp), ("coarse_b", vp), ("coarse_x", vp), ("perm0", vp),
                 ("in_stride", C.c_int32), ("cycle", C.c_int32), ("use_fcg", C.c_int32),
                 ("kwork", vp), ("kwork_len", C.c_int64), ("tail_start", C.c_int32),
-                ("tail_ctas", C.c_int32), ("tail_levels", vp), ("tail_colors", vp)]
+                ("tail_ctas", C.c_int32), ("tail_levels", vp), ("tail_colors", vp),
+                ("tail_phases", vp), ("tail_nphases", C.c_int32), ("pad_", C.c_int32)]
 
 
 class Wave(C.Structure):

@@ -252,7 +252,7 @@ def _permuted_rows_sell(A, perm: np.ndarray, inv: np.ndarray):
     return D.pack_sell(lane_row, lane_ptr, cols, vals, 1, n)
 
 
-TAIL_ROWS = 0  # levels at most this large run in the persistent tail kernel (0 = off; see DESIGN.md)
+TAIL_ROWS = 0  # levels at most this large run in the persistent tail kernel (0 = off; DESIGN.md section 4)
 
 
 class DeviceAmg:
@@ -351,8 +351,42 @@ class DeviceAmg:
         raw = np.frombuffer(bytes(arr), dtype=np.uint8).copy()
         self.tail_levels = D.upload(raw)
         self.tail_colors = D.upload(np.asarray(table, dtype=np.int32))
+        # phase table {type, level, colour, flags} (csrc/amg.cu TP_*): flags
+        # bit0 = zero-guess prefix, bit1 = snapshot colour (write tmp), bit2 = backward
+        GATHER, SWEEP, COPY, RR, COARSE, PROLONG, SCATTER, SEQ, ZERO = range(9)
+        ph = []
+        if ts == 0:
+            ph.append((GATHER, 0, 0, 0))
+
+        def smooth(l, backward):
+            dl = self.levels[l]
+            c = dl.desc.ncolors
+            if c == 1:
+                if not backward:
+                    ph.append((ZERO, l, 0, 0))
+                ph.append((SEQ, l, 0, 4 if backward else 0))
+                return
+            for q in range(c):
+                k = c - 1 - q if backward else q
+                snap = int(dl.snapshot[k]) if k < len(dl.snapshot) else 0
+                ph.append((SWEEP, l, k, (0 if backward else 1) | (2 * snap)))
+                if snap:
+                    ph.append((COPY, l, k, 0))
+
+        for l in range(ts, L - 1):
+            smooth(l, False)
+            ph.append((RR, l, 0, 0))
+        ph.append((COARSE, 0, 0, 0))
+        for l in range(L - 2, ts - 1, -1):
+            ph.append((PROLONG, l, 0, 0))
+            smooth(l, True)
+        if ts == 0:
+            ph.append((SCATTER, 0, 0, 0))
+        self.tail_phases = D.upload(np.asarray(ph, dtype=np.int32).reshape(-1))
         self.desc.tail_levels = D.ptr(self.tail_levels)
         self.desc.tail_colors = D.ptr(self.tail_colors)
+        self.desc.tail_phases = D.ptr(self.tail_phases)
+        self.desc.tail_nphases = len(ph)
         self.desc.tail_start = ts
 
     # -- V-cycle: one native call ------------------------------------------------

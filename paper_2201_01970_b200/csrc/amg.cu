@@ -377,7 +377,7 @@ __global__ void k_scatter(int n, const int32_t* __restrict__ idx, const double* 
 // cost is the number of dependent phases, not bandwidth.  Same arithmetic as
 // the per-colour kernels above (bit-identical results).
 // ---------------------------------------------------------------------------
-constexpr int TAIL_THREADS = 256;
+constexpr int TAIL_THREADS = 256;  // 255 registers: the next phase is held in registers
 
 struct TailCtx {
   int gtid, nthreads, gwarp, nwarps, lane, nctas;
@@ -461,50 +461,265 @@ __device__ __forceinline__ double dense_row_dot(const double* row, const double*
   return s;
 }
 
-__global__ void __launch_bounds__(TAIL_THREADS, 1)
-    k_vtail(const cprb_tail_level* __restrict__ lev, const int32_t* __restrict__ colors, int ts,
-            int nl, int n_coarse, const double* __restrict__ coarse_inv, double* coarse_b,
-            double* coarse_x, const double* r, int stride, const int32_t* __restrict__ perm0,
-            double* z, int nctas, unsigned long long* tlog) {
+// Phase-table driven tail (phases built by amg.DeviceAmg._build_tail):
+//   int32 [type, level, colour, flags] per phase.  Between phases every warp
+// already holds (in registers) the static data of its first work item of the
+// NEXT phase -- row lengths, slice bases, diagonal, up to TAIL_PF columns and
+// values -- so after the cluster barrier only the x gathers and b remain.
+enum { TP_GATHER = 0, TP_SWEEP = 1, TP_COPY = 2, TP_RR = 3, TP_COARSE = 4, TP_PROLONG = 5,
+       TP_SCATTER = 6, TP_SEQ = 7, TP_ZERO = 8 };
+constexpr int TAIL_PF = 16;
+
+struct TailPf {
+  int len, row, out, a;
+  int64_t base;
+  double d;
+  int col[TAIL_PF];
+  double val[TAIL_PF];
+};
+
+struct TailArgs {
+  const cprb_tail_level* lev;
+  const int32_t* colors;
+  const int4* phases;
+  int nphases;
+  int nl;
+  int n_coarse;
+  const double* coarse_inv;
+  double* coarse_b;
+  double* coarse_x;
+  const double* r;
+  int stride;
+  const int32_t* perm0;
+  double* z;
+};
+
+__device__ __forceinline__ void tail_prefetch(const TailCtx& t, const TailArgs& a, const int4 ph,
+                                              TailPf& pf) {
+  pf.len = 0;
+  pf.row = -1;
+  pf.out = -1;
+  if (ph.x == TP_SWEEP) {
+    const cprb_tail_level& L = a.lev[ph.y];
+    const int32_t* ct = a.colors + L.color_off;
+    const int nc = L.ncolors, k = ph.z;
+    const int s0 = ct[k], s1 = ct[k + 1];
+    const int r0 = ct[nc + 1 + k], r1 = ct[nc + 2 + k];
+    const int w = s0 + t.gwarp;
+    const int row = r0 + t.gwarp * 32 + t.lane;
+    if (w < s1 && row < r1) {
+      const int lid = w * 32 + t.lane;
+      pf.row = row;
+      pf.len = (ph.w & 1) ? __ldg(L.smoother.lane_len_lo + lid) : __ldg(L.smoother.lane_len + lid);
+      pf.base = __ldg(L.smoother.slice_ptr + w) + t.lane;
+      pf.d = __ldg(L.diag + row);
+#pragma unroll
+      for (int m = 0; m < TAIL_PF; ++m)
+        if (m < pf.len) {
+          pf.col[m] = __ldg(L.smoother.cols + pf.base + (int64_t)m * 32);
+          pf.val[m] = __ldg(L.smoother.vals + pf.base + (int64_t)m * 32);
+        }
+    }
+  } else if (ph.x == TP_RR) {
+    const cprb_sell& R = a.lev[ph.y].restrict_op;
+    const int w = t.gwarp;
+    if (w < R.nslices) {
+      const int lid = w * 32 + t.lane;
+      pf.row = __ldg(R.lane_row + lid);
+      pf.len = pf.row >= 0 ? __ldg(R.lane_len + lid) : 0;
+      pf.base = __ldg(R.slice_ptr + w) + t.lane;
+      pf.out = ((t.lane & 1) == 0) ? __ldg(R.agg_out + w * 16 + (t.lane >> 1)) : -1;
+#pragma unroll
+      for (int m = 0; m < TAIL_PF; ++m)
+        if (m < pf.len) {
+          pf.col[m] = __ldg(R.cols + pf.base + (int64_t)m * 32);
+          pf.val[m] = __ldg(R.vals + pf.base + (int64_t)m * 32);
+        }
+    }
+  } else if (ph.x == TP_PROLONG) {
+    const cprb_tail_level& L = a.lev[ph.y];
+    if (t.gtid < L.n) pf.a = __ldg(L.aggp + t.gtid);
+  }
+}
+
+// GS row from prefetched static data (pf) or straight from memory (first == false)
+__device__ __forceinline__ void tail_sweep_row(const cprb_tail_level& L, const double* x,
+                                               double* xout, int row, int len, int64_t base,
+                                               double d, const TailPf* pf) {
+  double acc = 0.0;
+  int m0 = 0;
+  if (pf) {
+    double xv[TAIL_PF];
+#pragma unroll
+    for (int m = 0; m < TAIL_PF; ++m) xv[m] = (m < len) ? __ldcg(x + pf->col[m]) : 0.0;
+    const double bi = __ldcg(L.b + row);
+#pragma unroll
+    for (int m = 0; m < TAIL_PF; ++m)
+      if (m < len) acc = acc + pf->val[m] * xv[m];
+    m0 = TAIL_PF;
+    if (len > m0) acc = gs_acc_from<16>(L.smoother, base, m0, len, x, acc);
+    xout[row] = (bi - acc) / d;
+    return;
+  }
+  (void)base;
+}
+
+__device__ __noinline__ void tail_sweep_rest(const TailCtx& t, const cprb_tail_level& L,
+                                             const int32_t* ct, int k, int flags) {
+  const int nc = L.ncolors;
+  const int s0 = ct[k], s1 = ct[k + 1];
+  const int r0 = ct[nc + 1 + k], r1 = ct[nc + 2 + k];
+  double* xout = (flags & 2) ? L.tmp : L.x;
+  for (int w = s0 + t.gwarp + t.nwarps; w < s1; w += t.nwarps) {
+    const int row = r0 + (w - s0) * 32 + t.lane;
+    if (row >= r1) continue;
+    const int lid = w * 32 + t.lane;
+    const int len = (flags & 1) ? __ldg(L.smoother.lane_len_lo + lid) : __ldg(L.smoother.lane_len + lid);
+    const double acc = gs_acc_from<16>(L.smoother, __ldg(L.smoother.slice_ptr + w) + t.lane, 0, len,
+                                       L.x, 0.0);
+    xout[row] = (__ldcg(L.b + row) - acc) / __ldg(L.diag + row);
+  }
+}
+
+__device__ __noinline__ void tail_rr_rest(const TailCtx& t, const cprb_sell& R, const double* b,
+                                          const double* x, double* bc) {
+  for (int w = t.gwarp + t.nwarps; w < R.nslices; w += t.nwarps) rr_slice(R, w, t.lane, b, x, bc);
+}
+
+__device__ __noinline__ double tail_rr_long(const cprb_sell& R, int64_t base, int len,
+                                            const double* x) {
+  return rr_row(R, base, 0, len, x);
+}
+
+__device__ __noinline__ void tail_coarse(const TailCtx& t, const TailArgs& a) {
+  for (int w = t.gwarp; w < a.n_coarse; w += t.nwarps) {
+    const double s = dense_row_dot(a.coarse_inv + (int64_t)w * a.n_coarse, a.coarse_b, a.n_coarse,
+                                   t.lane);
+    if (t.lane == 0) a.coarse_x[w] = s;
+  }
+}
+
+__device__ __noinline__ void tail_seq(const TailCtx& t, const cprb_tail_level& L, int backward) {
+  if (t.gtid != 0) return;
+  for (int q = 0; q < L.n; ++q) {
+    const int i = backward ? L.n - 1 - q : q;
+    const int w = i >> 5, lane = i & 31;
+    const int len = L.smoother.lane_len[w * 32 + lane];
+    const int64_t base = L.smoother.slice_ptr[w] + lane;
+    double acc = 0.0;
+    for (int m = 0; m < len; ++m) {
+      const int64_t e = base + (int64_t)m * 32;
+      acc = acc + L.smoother.vals[e] * __ldcg(L.x + L.smoother.cols[e]);
+    }
+    L.x[i] = (__ldcg(L.b + i) - acc) / L.diag[i];
+  }
+}
+
+__device__ __forceinline__ void tail_exec(const TailCtx& t, const TailArgs& a, const int4 ph,
+                                          const TailPf& pf) {
+  switch (ph.x) {
+    case TP_GATHER: {
+      const cprb_tail_level& L = a.lev[0];
+      for (int i = t.gtid; i < L.n; i += t.nthreads)
+        L.b[i] = a.r[(int64_t)a.stride * __ldg(a.perm0 + i)];
+      break;
+    }
+    case TP_SWEEP: {
+      const cprb_tail_level& L = a.lev[ph.y];
+      const int32_t* ct = a.colors + L.color_off;
+      const int nc = L.ncolors, k = ph.z;
+      const int s0 = ct[k], s1 = ct[k + 1];
+      const int r0 = ct[nc + 1 + k], r1 = ct[nc + 2 + k];
+      double* xout = (ph.w & 2) ? L.tmp : L.x;
+      if (pf.row >= 0) tail_sweep_row(L, L.x, xout, pf.row, pf.len, pf.base, pf.d, &pf);
+      if (s1 - s0 > t.nwarps) tail_sweep_rest(t, L, ct, k, ph.w);
+      (void)r0;
+      (void)r1;
+      break;
+    }
+    case TP_COPY: {
+      const cprb_tail_level& L = a.lev[ph.y];
+      const int32_t* ct = a.colors + L.color_off;
+      const int nc = L.ncolors, k = ph.z;
+      for (int i = ct[nc + 1 + k] + t.gtid; i < ct[nc + 2 + k]; i += t.nthreads) L.x[i] = __ldcg(L.tmp + i);
+      break;
+    }
+    case TP_RR: {
+      const cprb_tail_level& L = a.lev[ph.y];
+      const cprb_sell& R = L.restrict_op;
+      double* bc = (ph.y + 1 < a.nl - 1) ? a.lev[ph.y + 1].b : a.coarse_b;
+      if (t.gwarp < R.nslices) {
+        double res = 0.0;
+        if (pf.row >= 0) {
+          double t2;
+          if (pf.len <= TAIL_PF) {
+            double e[TAIL_PF];
+#pragma unroll
+            for (int m = 0; m < TAIL_PF; ++m) e[m] = (m < pf.len) ? pf.val[m] * __ldcg(L.x + pf.col[m]) : 0.0;
+            t2 = segsum_masked<TAIL_PF>(e, pf.len);
+          } else {
+            t2 = tail_rr_long(R, pf.base, pf.len, L.x);
+          }
+          res = __ldcg(L.b + pf.row) - t2;
+        }
+        const double other = __shfl_down_sync(CPRB_FULL, res, 1);
+        if ((t.lane & 1) == 0 && pf.out >= 0) bc[pf.out] = (0.0 + res) + other;
+      }
+      if (R.nslices > t.nwarps) tail_rr_rest(t, R, L.b, L.x, bc);
+      break;
+    }
+    case TP_COARSE:
+      tail_coarse(t, a);
+      break;
+    case TP_PROLONG: {
+      const cprb_tail_level& L = a.lev[ph.y];
+      const double* xc = (ph.y + 1 < a.nl - 1) ? a.lev[ph.y + 1].x : a.coarse_x;
+      if (t.gtid < L.n) L.x[t.gtid] = __ldcg(L.x + t.gtid) + __ldcg(xc + pf.a);
+      for (int i = t.gtid + t.nthreads; i < L.n; i += t.nthreads)
+        L.x[i] = __ldcg(L.x + i) + __ldcg(xc + __ldg(L.aggp + i));
+      break;
+    }
+    case TP_SCATTER: {
+      const cprb_tail_level& L = a.lev[0];
+      for (int i = t.gtid; i < L.n; i += t.nthreads) a.z[__ldg(a.perm0 + i)] = __ldcg(L.x + i);
+      break;
+    }
+    case TP_ZERO: {
+      const cprb_tail_level& L = a.lev[ph.y];
+      for (int i = t.gtid; i < L.n; i += t.nthreads) L.x[i] = 0.0;
+      break;
+    }
+    case TP_SEQ:  // single-colour level: classic sequential GS (src/smoothers.py:296-299)
+      tail_seq(t, a.lev[ph.y], ph.w & 4);
+      break;
+    default:
+      break;
+  }
+}
+
+__global__ void __launch_bounds__(TAIL_THREADS, 1) k_vtail(const TailArgs a, int nctas,
+                                                            unsigned long long* tlog) {
   TailCtx t;
   int tn = 0;
   t.tlog = tlog;
   t.tn = &tn;
-  if (tlog && t.gtid == 0) tlog[tn++] = gtimer();
   t.nctas = nctas;
   t.gtid = blockIdx.x * blockDim.x + threadIdx.x;
   t.nthreads = gridDim.x * blockDim.x;
   t.gwarp = t.gtid >> 5;
   t.nwarps = t.nthreads >> 5;
   t.lane = threadIdx.x & 31;
-  if (ts == 0) {  // whole cycle in the tail: CPR restriction r[stride * perm]
-    const cprb_tail_level& L = lev[0];
-    for (int i = t.gtid; i < L.n; i += t.nthreads) L.b[i] = r[(int64_t)stride * __ldg(perm0 + i)];
-    tail_sync(t);
-  }
-  for (int l = ts; l < nl - 1; ++l) {
-    const cprb_tail_level& L = lev[l];
-    tail_pass(t, L, colors + L.color_off, 0, true);
-    double* bc = (l + 1 < nl - 1) ? lev[l + 1].b : coarse_b;
-    for (int w = t.gwarp; w < L.restrict_op.nslices; w += t.nwarps)
-      rr_slice(L.restrict_op, w, t.lane, L.b, L.x, bc);
-    tail_sync(t);
-  }
-  for (int w = t.gwarp; w < n_coarse; w += t.nwarps) {
-    const double s = dense_row_dot(coarse_inv + (int64_t)w * n_coarse, coarse_b, n_coarse, t.lane);
-    if (t.lane == 0) coarse_x[w] = s;
-  }
-  tail_sync(t);
-  for (int l = nl - 2; l >= ts; --l) {
-    const cprb_tail_level& L = lev[l];
-    const double* xc = (l + 1 < nl - 1) ? lev[l + 1].x : coarse_x;
-    for (int i = t.gtid; i < L.n; i += t.nthreads) L.x[i] = __ldcg(L.x + i) + __ldcg(xc + __ldg(L.aggp + i));
-    tail_sync(t);
-    tail_pass(t, L, colors + L.color_off, 1, false);
-  }
-  if (ts == 0) {
-    const cprb_tail_level& L = lev[0];
-    for (int i = t.gtid; i < L.n; i += t.nthreads) z[__ldg(perm0 + i)] = __ldcg(L.x + i);
+  if (tlog && t.gtid == 0) tlog[tn++] = gtimer();
+  TailPf pf;
+  int4 ph = a.nphases > 0 ? __ldg(a.phases) : make_int4(-1, 0, 0, 0);
+  tail_prefetch(t, a, ph, pf);
+  for (int p = 0; p < a.nphases; ++p) {
+    tail_exec(t, a, ph, pf);
+    if (p + 1 < a.nphases) {
+      ph = __ldg(a.phases + p + 1);
+      tail_prefetch(t, a, ph, pf);  // static loads stay in flight across the barrier
+      tail_sync(t);
+    }
   }
 }
 
@@ -584,9 +799,21 @@ static int launch_vtail(const cprb_amg& h, const double* r, double* z, cudaStrea
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k_vtail, h.tail_levels, h.tail_colors, h.tail_start,
-                                     h.nlevels, h.n_coarse, h.coarse_inv, h.coarse_b, h.coarse_x, r,
-                                     h.in_stride, h.perm0, z, g, tlog);
+  TailArgs ta;
+  ta.lev = h.tail_levels;
+  ta.colors = h.tail_colors;
+  ta.phases = reinterpret_cast<const int4*>(h.tail_phases);
+  ta.nphases = h.tail_nphases;
+  ta.nl = h.nlevels;
+  ta.n_coarse = h.n_coarse;
+  ta.coarse_inv = h.coarse_inv;
+  ta.coarse_b = h.coarse_b;
+  ta.coarse_x = h.coarse_x;
+  ta.r = r;
+  ta.stride = h.in_stride;
+  ta.perm0 = h.perm0;
+  ta.z = z;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_vtail, ta, g, tlog);
   if (e != cudaSuccess)
     return set_error(CPRB_EDEVICE, std::string("v-cycle tail launch: ") + cudaGetErrorString(e));
   return check_launch("v-cycle tail");
@@ -654,7 +881,8 @@ int amg_vcycle(const cprb_amg& h, const double* r, double* z, cudaStream_t st) {
                                                                      h.coarse_b, z, nullptr);
     return check_launch("coarse-only cycle");
   }
-  const bool tail = h.tail_levels && h.tail_colors && h.tail_start >= 0 && h.tail_start < nl - 1;
+  const bool tail = h.tail_levels && h.tail_colors && h.tail_phases && h.tail_nphases > 0 &&
+                    h.tail_start >= 0 && h.tail_start < nl - 1;
   const int ts = tail ? h.tail_start : nl - 1;
   for (int l = 0; l < ts; ++l) {
     const cprb_amg_level& L = h.levels[l];
