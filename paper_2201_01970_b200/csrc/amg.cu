@@ -258,7 +258,8 @@ __device__ __forceinline__ void rr_slice(const cprb_sell& R, int w, int lane, co
 template <int PRE>
 __global__ void __launch_bounds__(256)
     k_resid_restrict(const cprb_sell R, const double* __restrict__ b,
-                     const double* __restrict__ x, double* __restrict__ bc) {
+                     const double* __restrict__ x, double* __restrict__ bc,
+                     double* __restrict__ xn, const double* __restrict__ dn, int c0_rows) {
   pdl_trigger();
   AmgMark mk;
   mk.start(3);
@@ -299,19 +300,31 @@ __global__ void __launch_bounds__(256)
     res = __ldcg(b + row) - t;
   }
   const double other = __shfl_down_sync(CPRB_FULL, res, 1);
-  if ((lane & 1) == 0 && out >= 0) bc[out] = (0.0 + res) + other;
+  if ((lane & 1) == 0 && out >= 0) {
+    const double bcv = (0.0 + res) + other;
+    bc[out] = bcv;
+    // fused first colour of the next level's zero-guess forward sweep: its
+    // rows read no x (no earlier colour), so x = (b - 0.0) / d exactly as
+    // k_sweep computes it (src/smoothers.py:106-115)
+    if (xn && out < c0_rows) xn[out] = (bcv - 0.0) / dn[out];
+  }
   mk.end();
 }
 
+// `next` (optional): the next (smoothed, multi-colour) level whose zero-guess
+// first colour is computed by this kernel
 static void launch_rr(const cprb_amg_level& L, const double* b, const double* x, double* bc,
-                      cudaStream_t st) {
+                      cudaStream_t st, const cprb_amg_level* next = nullptr) {
   const cprb_sell& R = L.restrict_op;
   if (R.nslices <= 0) return;
   const int grid = nblk((int64_t)R.nslices * 32, 256);
   const int wdt = L.restrict_width > 0 ? L.restrict_width : 32;
-  if (wdt <= 8) launch_pdl(k_resid_restrict<8>, grid, 256, 0, st, R, b, x, bc);
-  else if (wdt <= 16) launch_pdl(k_resid_restrict<16>, grid, 256, 0, st, R, b, x, bc);
-  else launch_pdl(k_resid_restrict<32>, grid, 256, 0, st, R, b, x, bc);
+  double* xn = next ? next->x : nullptr;
+  const double* dn = next ? next->diag : nullptr;
+  const int c0 = next ? next->color_rows[1] : 0;
+  if (wdt <= 8) launch_pdl(k_resid_restrict<8>, grid, 256, 0, st, R, b, x, bc, xn, dn, c0);
+  else if (wdt <= 16) launch_pdl(k_resid_restrict<16>, grid, 256, 0, st, R, b, x, bc, xn, dn, c0);
+  else launch_pdl(k_resid_restrict<32>, grid, 256, 0, st, R, b, x, bc, xn, dn, c0);
 }
 
 // prolongation-correct x += ec[agg]  (src/amg.py:264)
@@ -840,7 +853,7 @@ static void launch_sweep(const cprb_amg_level& L, int k, double* b, const double
 
 int pgs_pass(const cprb_amg_level& L, const double* b_in, double* x, int dir, int zero_guess,
              const double* gsrc, int gstride, const int32_t* perm, double* sout,
-             cudaStream_t st) {
+             cudaStream_t st, int skip_first) {
   double* b = const_cast<double*>(b_in);
   const int c = L.ncolors;
   if (c == 1) {
@@ -850,7 +863,7 @@ int pgs_pass(const cprb_amg_level& L, const double* b_in, double* x, int dir, in
     if (sout) k_scatter<<<nblk(L.n, 256), 256, 0, st>>>(L.n, perm, x, sout);
     return check_launch("pgs sequential");
   }
-  for (int t = 0; t < c; ++t) {
+  for (int t = skip_first; t < c; ++t) {
     const int k = dir ? c - 1 - t : t;
     const int s0 = L.color_slices[k], s1 = L.color_slices[k + 1];
     const bool snap = L.color_snapshot && L.color_snapshot[k];
@@ -884,12 +897,16 @@ int amg_vcycle(const cprb_amg& h, const double* r, double* z, cudaStream_t st) {
   const bool tail = h.tail_levels && h.tail_colors && h.tail_phases && h.tail_nphases > 0 &&
                     h.tail_start >= 0 && h.tail_start < nl - 1;
   const int ts = tail ? h.tail_start : nl - 1;
+  int fused = 0;  // colour 0 of this level was computed by the previous restriction
   for (int l = 0; l < ts; ++l) {
     const cprb_amg_level& L = h.levels[l];
-    int rc = pgs_pass(L, L.b, L.x, 0, 1, l == 0 ? r : nullptr, h.in_stride, h.perm0, nullptr, st);
+    int rc = pgs_pass(L, L.b, L.x, 0, 1, l == 0 ? r : nullptr, h.in_stride, h.perm0, nullptr, st,
+                      fused);
     if (rc) return rc;
     double* bc = (l + 1 < nl - 1) ? h.levels[l + 1].b : h.coarse_b;
-    launch_rr(L, L.b, L.x, bc, st);
+    const cprb_amg_level* next = (l + 1 < ts && h.levels[l + 1].ncolors > 1) ? &h.levels[l + 1] : nullptr;
+    launch_rr(L, L.b, L.x, bc, st, next);
+    fused = next ? 1 : 0;
   }
   if (tail) {
     int rc = launch_vtail(h, r, z, st);

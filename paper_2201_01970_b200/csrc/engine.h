@@ -43,5 +43,5 @@ int bilu_solve(const cprb_bilu& F, const double* r, double* zl, double* y, const
 int fill_sentinel(double* p, int64_t n, cudaStream_t st);
 int pgs_pass(const cprb_amg_level& L, const double* b, double* x, int dir, int zero_guess,
              const double* gather_src, int gather_stride, const int32_t* perm,
-             double* scatter_out, cudaStream_t st);
+             double* scatter_out, cudaStream_t st, int skip_first = 0);
 }  // namespace cprb
