@@ -255,8 +255,15 @@ __device__ __forceinline__ void rr_slice(const cprb_sell& R, int w, int lane, co
 // standalone launch: the static part of the slice (columns, values, output
 // slots) is fetched before the PDL wait; rows longer than PRE fall back to
 // the streaming sum.
+// long rows (> PRE entries) leave the register path: kept out of line so the
+// common case is not charged the fallback's registers
+__device__ __noinline__ double rr_row_far(const cprb_sell& R, int64_t base, int len,
+                                          const double* x) {
+  return rr_row(R, base, 0, len, x);
+}
+
 template <int PRE>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, PRE <= 16 ? 4 : 2)
     k_resid_restrict(const cprb_sell R, const double* __restrict__ b,
                      const double* __restrict__ x, double* __restrict__ bc,
                      double* __restrict__ xn, const double* __restrict__ dn, int c0_rows) {
@@ -295,7 +302,7 @@ __global__ void __launch_bounds__(256)
       for (int m = 0; m < PRE; ++m) e[m] = (m < len) ? v[m] * __ldcg(x + c[m]) : 0.0;
       t = segsum_masked<PRE>(e, len);
     } else {
-      t = rr_row(R, base, 0, len, x);
+      t = rr_row_far(R, base, len, x);
     }
     res = __ldcg(b + row) - t;
   }
