@@ -262,9 +262,12 @@ def run_ours(args):
     dom = max(share, key=share.get)
     dus, dbytes = kern[dom]
     achieved = dbytes / (dus * 1e-6) / 1e9
+    traffic, traffic_src = _ncu_traffic(dom)
     roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
                 "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                "traffic": None, "share_of_step": round(share[dom] * 1e-3 / ms, 3)}
+                "traffic": traffic, "traffic_source": traffic_src,
+                "algorithmic_bytes": int(dbytes),
+                "share_of_step": round(share[dom] * 1e-3 / ms, 3)}
 
     launches_per_solve, kernel_names = _count_launches(solve, torch)
     out = {
@@ -293,6 +296,20 @@ def run_ours(args):
         print(json.dumps(out))
     if ws > 1:
         dist.destroy_process_group()
+
+
+def _ncu_traffic(kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`
+    (a bench kernel family) from the committed ncu --set full capture
+    summarised in profiles/ (tools/ncu_summary.py); None if absent."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if not p.exists():
+        return None, None
+    d = json.loads(p.read_text())
+    e = d.get("kernels", {}).get(kernel)
+    if not e:
+        return None, None
+    return int(e["dram_bytes"]), d.get("source")
 
 
 def _count_launches(solve, torch):

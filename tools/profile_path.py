@@ -125,6 +125,22 @@ def main():
             lag = [(L[u, c, 100] - L[u, c - 1, 100]) / 1e3 for c in range(1, nch) if L[u, c, 100] > 0]
             print(" lag@step100 median", np.median(lag), "first", lag[:5])
         return
+    if a.what in ("vcyclecold", "bilucold"):
+        t = torch
+        flush = t.empty(64 * 1024 * 1024, dtype=t.float64, device="cuda")   # 512 MB > L2
+        g = ops["vcycleg"] if a.what == "vcyclecold" else ops["bilu"]
+        e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+        tot = 0.0
+        for rep in range(a.reps + 2):
+            flush.fill_(1.0)
+            e0.record()
+            g()
+            e1.record()
+            t.cuda.synchronize()
+            if rep >= 2:
+                tot += e0.elapsed_time(e1)
+        print(f"{a.what}: {tot / a.reps:.3f} ms/rep (device, L2 flushed before each rep)")
+        return
     fn = ops[a.what]
     fn()
     torch.cuda.synchronize()
