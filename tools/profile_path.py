@@ -38,6 +38,10 @@ def main():
         "spmv": lambda: P.spmv(A, bd),
         "bilu": lambda: Bd.bilu.apply(bd, z),
         "vcycle": lambda: Bd.amg.vcycle(bd, zp),
+        "finish": lambda: N.check(N.lib().cprb_cpr_finish(C.byref(Bd.desc), D.ptr(bd), D.ptr(z),
+                                                          D.stream())),
+        "applynog": lambda: N.check(N.lib().cprb_cpr_apply(C.byref(Bd.desc), D.ptr(bd), D.ptr(z),
+                                                           D.stream())),
         "vcycleg": lambda: N.check(N.lib().cprb_amg_cycle_graph(Bd.graphs, C.byref(Bd.amg.desc),
                                                                 D.ptr(bd), D.ptr(zp), D.stream())),
         "solve": lambda: P.gmres_solve(A, bd, None, B, cfg.gmres_params()),
