@@ -204,7 +204,12 @@ typedef struct cprb_bilu {
   cprb_wave Uw;
   const int32_t* l_slot;       /* dev, n: rhs slot of each row in the L plan */
   double* rhs_l;               /* dev work: rhs in L step order */
-  double* rhs_u;               /* dev work: z in U step order */
+  double* rhs_u;               /* dev work: z in U step order (U solve input) */
+  const int32_t* u_slot;       /* dev, n: rhs slot of each row in the U plan */
+  double* zl_step;             /* dev work: z in L step order (L output, sentinel-polled) */
+  double* y_step;              /* dev work: y in U step order (U output, sentinel-polled) */
+  int64_t len_l;               /* doubles in rhs_l / zl_step */
+  int64_t len_u;               /* doubles in rhs_u / y_step */
 } cprb_bilu;
 
 typedef struct cprb_cpr {

@@ -64,7 +64,8 @@ class Wave(C.Structure):
 class Bilu(C.Structure):
     _fields_ = [("n", C.c_int32), ("b", C.c_int32), ("L", Sell), ("U", Sell), ("uinv", vp),
                 ("tickets", vp), ("use_wave", C.c_int32), ("Lw", Wave), ("Uw", Wave),
-                ("l_slot", vp), ("rhs_l", vp), ("rhs_u", vp)]
+                ("l_slot", vp), ("rhs_l", vp), ("rhs_u", vp), ("u_slot", vp), ("zl_step", vp),
+                ("y_step", vp), ("len_l", C.c_int64), ("len_u", C.c_int64)]
 
 
 class Cpr(C.Structure):

@@ -185,11 +185,16 @@ extern "C" int cprb_bilu_apply(const cprb_bilu* F, const double* r, double* z, d
   int rc = fill_sentinel(work_l, n, st);
   if (rc) return rc;
   if (F->use_wave) {
-    rc = fill_sentinel(z, n, st);  // the U solve polls its own output
+    // the solves poll their own step-ordered outputs
+    rc = fill_sentinel(F->zl_step, F->len_l, st);
+    if (rc) return rc;
+    rc = fill_sentinel(F->y_step, F->len_u, st);
     if (rc) return rc;
     rc = wave_scatter_rhs(*F, r, F->rhs_l, st);
     if (rc) return rc;
-    return wave_solve(*F, F->rhs_l, work_l, F->rhs_u, z, nullptr, nullptr, st);
+    rc = wave_solve(*F, F->rhs_l, st);
+    if (rc) return rc;
+    return wave_combine(*F, nullptr, z, st);
   }
   return bilu_solve(*F, r, work_l, z, nullptr, nullptr, st);
 }

@@ -33,9 +33,10 @@ int check_launch(const char* what);
 
 int bsr_op(int mode, const cprb_sell& A, int b, const double* x, const double* rhs, double* out,
            int32_t* flag, double* sent, cudaStream_t st, const int32_t* out_idx = nullptr,
-           double* sent2 = nullptr);
-int wave_solve(const cprb_bilu& F, const double* rhsL, double* zl, double* zu_rhs, double* y,
-               const double* zp, double* zout, cudaStream_t st);
+           double* sent2 = nullptr, const int32_t* sent_idx = nullptr,
+           const int32_t* sent2_idx = nullptr);
+int wave_solve(const cprb_bilu& F, const double* rhsL, cudaStream_t st);
+int wave_combine(const cprb_bilu& F, const double* zp, double* z, cudaStream_t st);
 int wave_scatter_rhs(const cprb_bilu& F, const double* r, double* rhsL, cudaStream_t st);
 int amg_vcycle(const cprb_amg& h, const double* r, double* z, cudaStream_t st);
 int bilu_solve(const cprb_bilu& F, const double* r, double* zl, double* y, const double* zp,

@@ -120,21 +120,6 @@ __global__ void k_gemv_t(int64_t n, int k, const double* __restrict__ V, int64_t
   }
 }
 
-// src/cpr.py:184-186  z = prolong(zp) + y:  z[b i] = zp[i] + y[b i],
-// z[b i + c] = 0.0 + y[b i + c]  (the zeros of the prolongation are added)
-__global__ void k_combine_pressure(int64_t nb, int b, const double* __restrict__ zp,
-                                   const double* __restrict__ y, double* __restrict__ z) {
-  pdl_trigger();
-  pdl_wait();
-  const int64_t n = nb * b;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t cell = i / b;
-    const double base = (i - cell * b == 0) ? zp[cell] : 0.0;
-    z[i] = base + y[i];
-  }
-}
-
 __global__ void k_add(int64_t n, const double* __restrict__ x, const double* __restrict__ s,
                       double* __restrict__ out) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
@@ -242,18 +227,16 @@ int cprb_cpr_finish(const cprb_cpr* P, const double* r, double* z, void* stream)
   cudaStream_t st = (cudaStream_t)stream;
   const cprb_bilu& F = P->bilu;
   if (F.use_wave) {
-    // stage-2 residual written straight into the L plan's step order
-    // (also arms zl and y, the sentinel-polled outputs of the L and U solves)
-    int rc = bsr_op(2, P->A, P->b, P->zp, r, F.rhs_l, nullptr, P->zl, st, F.l_slot, P->y);
+    // stage-2 residual written straight into the L plan's step order; it
+    // also arms the step-ordered outputs the L and U solves poll
+    int rc = bsr_op(2, P->A, P->b, P->zp, r, F.rhs_l, nullptr, F.zl_step, st, F.l_slot, F.y_step,
+                    F.l_slot, F.u_slot);
     if (rc) return rc;
-    // the U solve only publishes y; z = Pi zp + y is a separate coalesced
-    // pass (a scattered zp load + store per row would sit on the U solve's
-    // per-step critical path)
-    rc = wave_solve(F, F.rhs_l, P->zl, F.rhs_u, P->y, nullptr, nullptr, st);
+    // the solves publish in step order (coalesced); z = Pi zp + y is one
+    // gather pass afterwards
+    rc = wave_solve(F, F.rhs_l, st);
     if (rc) return rc;
-    launch_pdl(k_combine_pressure, ew_blocks((int64_t)P->nb * P->b), 256, 0, st,
-               (int64_t)P->nb, P->b, (const double*)P->zp, (const double*)P->y, z);
-    return check_launch("cpr combine");
+    return wave_combine(F, P->zp, z, st);
   }
   int rc = bsr_op(2, P->A, P->b, P->zp, r, P->r2, nullptr, P->zl, st);  // also arms zl
   if (rc) return rc;

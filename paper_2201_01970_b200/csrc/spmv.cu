@@ -66,7 +66,8 @@ template <int B, int MODE>
 __global__ void __launch_bounds__(BSR_WARPS * 32, 4)
     k_bsr(const cprb_sell A, const double* __restrict__ x, const double* __restrict__ rhs,
           double* __restrict__ out, int32_t* flag, double* __restrict__ sent,
-          double* __restrict__ sent2, const int32_t* __restrict__ out_idx) {
+          double* __restrict__ sent2, const int32_t* __restrict__ out_idx,
+          const int32_t* __restrict__ sent_idx, const int32_t* __restrict__ sent2_idx) {
   pdl_trigger();
   const int gw = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
@@ -97,32 +98,34 @@ __global__ void __launch_bounds__(BSR_WARPS * 32, 4)
   if (MODE != 0) v = rhs[o] - v;
   const int64_t ob = out_idx ? (int64_t)out_idx[row] + r : o;
   out[ob] = v;
-  if (MODE == 2 && sent) sent[o] = sentinel();
-  if (MODE == 2 && sent2) sent2[o] = sentinel();
+  if (MODE == 2 && sent) sent[sent_idx ? (int64_t)sent_idx[row] + r : o] = sentinel();
+  if (MODE == 2 && sent2) sent2[sent2_idx ? (int64_t)sent2_idx[row] + r : o] = sentinel();
   flag_nonfinite(flag, !isfinite(v));
 }
 
 template <int B, int MODE>
 static void launch_bsr(const cprb_sell& A, const double* x, const double* rhs, double* out,
                        int32_t* flag, double* sent, double* sent2, cudaStream_t st,
-                       const int32_t* oi) {
+                       const int32_t* oi, const int32_t* si, const int32_t* si2) {
   if (A.nslices <= 0) return;
   const int threads = BSR_WARPS * 32;
   const int64_t warps = (int64_t)A.nslices * B;
   const int blocks = (int)((warps + BSR_WARPS - 1) / BSR_WARPS);
-  launch_pdl(k_bsr<B, MODE>, blocks, threads, 0, st, A, x, rhs, out, flag, sent, sent2, oi);
+  launch_pdl(k_bsr<B, MODE>, blocks, threads, 0, st, A, x, rhs, out, flag, sent, sent2, oi, si,
+             si2);
 }
 
 int bsr_op(int mode, const cprb_sell& A, int b, const double* x, const double* rhs, double* out,
-           int32_t* flag, double* sent, cudaStream_t st, const int32_t* oi, double* sent2) {
+           int32_t* flag, double* sent, cudaStream_t st, const int32_t* oi, double* sent2,
+           const int32_t* si, const int32_t* si2) {
   if (b == 3) {
-    if (mode == 0) launch_bsr<3, 0>(A, x, rhs, out, flag, sent, sent2, st, oi);
-    else if (mode == 1) launch_bsr<3, 1>(A, x, rhs, out, flag, sent, sent2, st, oi);
-    else launch_bsr<3, 2>(A, x, rhs, out, flag, sent, sent2, st, oi);
+    if (mode == 0) launch_bsr<3, 0>(A, x, rhs, out, flag, sent, sent2, st, oi, si, si2);
+    else if (mode == 1) launch_bsr<3, 1>(A, x, rhs, out, flag, sent, sent2, st, oi, si, si2);
+    else launch_bsr<3, 2>(A, x, rhs, out, flag, sent, sent2, st, oi, si, si2);
   } else if (b == 1) {
-    if (mode == 0) launch_bsr<1, 0>(A, x, rhs, out, flag, sent, sent2, st, oi);
-    else if (mode == 1) launch_bsr<1, 1>(A, x, rhs, out, flag, sent, sent2, st, oi);
-    else launch_bsr<1, 2>(A, x, rhs, out, flag, sent, sent2, st, oi);
+    if (mode == 0) launch_bsr<1, 0>(A, x, rhs, out, flag, sent, sent2, st, oi, si, si2);
+    else if (mode == 1) launch_bsr<1, 1>(A, x, rhs, out, flag, sent, sent2, st, oi, si, si2);
+    else launch_bsr<1, 2>(A, x, rhs, out, flag, sent, sent2, st, oi, si, si2);
   } else {
     return set_error(CPRB_EUNSUPPORTED, "block size " + std::to_string(b) + " not supported on device");
   }

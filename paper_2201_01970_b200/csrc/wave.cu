@@ -176,12 +176,12 @@ __device__ __forceinline__ void row_fast(uint32_t sblk, uint32_t srhs, int l, in
   for (int m = 0; m < K; ++m)
     if (m < len && code[m] >= 0)
 #pragma unroll
-      for (int c = 0; c < B; ++c) dv[m][c] = ld_relaxed(glob + (int64_t)B * code[m] + c);
+      for (int c = 0; c < B; ++c) dv[m][c] = ld_relaxed(glob + (int64_t)code[m] + c);
 #pragma unroll
   for (int m = 0; m < K; ++m) {
     if (m < len) {
       if (code[m] < 0) ring_value<B>(ring, k, -code[m] - 1, dv[m]);
-      else wait_block<B>(glob + (int64_t)B * code[m], dv[m]);
+      else wait_block<B>(glob + (int64_t)code[m], dv[m]);
     } else {
 #pragma unroll
       for (int c = 0; c < B; ++c) dv[m][c] = 0.0;
@@ -231,8 +231,8 @@ __device__ __noinline__ void row_general(const uint8_t* blk, int K, const double
         ring_value<B>(ring, k, -code - 1, dv);
       } else {
 #pragma unroll
-        for (int c = 0; c < B; ++c) dv[c] = ld_relaxed(glob + (int64_t)B * code + c);
-        wait_block<B>(glob + (int64_t)B * code, dv);
+        for (int c = 0; c < B; ++c) dv[c] = ld_relaxed(glob + (int64_t)code + c);
+        wait_block<B>(glob + (int64_t)code, dv);
       }
       double mr[B];
 #pragma unroll
@@ -254,15 +254,13 @@ __device__ __noinline__ void row_general(const uint8_t* blk, int K, const double
   }
 }
 
-// UPPER = false: z = r - sum L z   (publishes exported z rows, copies z into
-//                the U plan's rhs order via aux slots; y must be armed with
-//                the sentinel by the caller)
-// UPPER = true : y = Uinv (z - sum U y); final = z1 + y
+// UPPER = false: z = r - sum L z         (z published in L-step order)
+// UPPER = true : y = Uinv (z - sum U y)   (y published in U-step order)
+// out_step must hold the sentinel (armed by the caller) wherever it is polled.
 template <int B, bool UPPER>
 __global__ void __launch_bounds__(WAVE_THREADS, 1)
-    k_wave(const cprb_wave W, const double* __restrict__ rhs_steps, double* out_nat,
-           double* __restrict__ next_rhs, const double* __restrict__ zp,
-           double* __restrict__ final_out, int32_t* ticket) {
+    k_wave(const cprb_wave W, const double* __restrict__ rhs_steps, double* out_step,
+           int32_t* ticket) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   __shared__ StepMeta s_meta[WAVE_META];
   __shared__ __align__(8) uint64_t s_full[WAVE_NWARPS][WAVE_DEPTH];
@@ -372,24 +370,19 @@ __global__ void __launch_bounds__(WAVE_THREADS, 1)
         if (pos < mk.w) {
           const uint8_t* gblk = W.stream + mk.off + (int64_t)warp * mk.bytes;
           const double* grhs = rhs_steps + mk.rhs_off + warp * 32 * B;
-          const int row = fast ? lds_s32(sblk + 4u * lane) : reinterpret_cast<const int32_t*>(gblk)[lane];
           const int lenw = fast ? lds_s32(sblk + 4u * (32 + lane))
                                 : reinterpret_cast<const int32_t*>(gblk)[32 + lane];
-          const int aux = UPPER ? 0
-                                : (fast ? lds_s32(sblk + 4u * (64 + lane))
-                                        : reinterpret_cast<const int32_t*>(gblk)[64 + lane]);
           const int len = lenw & WAVE_LEN_MASK;
-          const bool publish = (lenw & WAVE_EXPORT) || (UPPER && !final_out);
           double res[B];
           if (fast) {
             switch (mk.k) {
-              case 0: row_fast<B, UPPER, 0>(sblk, srhs, lane, len, ring, k, out_nat, res); break;
-              case 1: row_fast<B, UPPER, 1>(sblk, srhs, lane, len, ring, k, out_nat, res); break;
-              case 2: row_fast<B, UPPER, 2>(sblk, srhs, lane, len, ring, k, out_nat, res); break;
-              default: row_fast<B, UPPER, 3>(sblk, srhs, lane, len, ring, k, out_nat, res); break;
+              case 0: row_fast<B, UPPER, 0>(sblk, srhs, lane, len, ring, k, out_step, res); break;
+              case 1: row_fast<B, UPPER, 1>(sblk, srhs, lane, len, ring, k, out_step, res); break;
+              case 2: row_fast<B, UPPER, 2>(sblk, srhs, lane, len, ring, k, out_step, res); break;
+              default: row_fast<B, UPPER, 3>(sblk, srhs, lane, len, ring, k, out_step, res); break;
             }
           } else {
-            row_general<B, UPPER>(gblk, mk.k, grhs, lane, len, ring, k, out_nat, res);
+            row_general<B, UPPER>(gblk, mk.k, grhs, lane, len, ring, k, out_step, res);
           }
           const uint32_t slot = (uint32_t)((k % WAVE_RING) * WAVE_THREADS + pos);
 #pragma unroll
@@ -400,22 +393,13 @@ __global__ void __launch_bounds__(WAVE_THREADS, 1)
           } else {
             sts_release_s32(ring.flag + 4u * slot, k);
           }
+          // publish in step order: one contiguous, coalesced row block per
+          // warp (the next chunk's polls, the U solve's input and the final
+          // combine all read this array)
           if (!(mode & 2)) {
-          if (publish) {
+            double* o = out_step + mk.rhs_off + (int64_t)pos * B;
 #pragma unroll
-            for (int r = 0; r < B; ++r) st_relaxed(out_nat + (int64_t)B * row + r, res[r]);
-          }
-          if constexpr (!UPPER) {
-#pragma unroll
-            for (int r = 0; r < B; ++r) next_rhs[(int64_t)aux + r] = res[r];
-          } else {
-            if (final_out) {
-              const double z1 = zp ? zp[row] : 0.0;
-#pragma unroll
-              for (int r = 0; r < B; ++r)
-                final_out[(int64_t)B * row + r] = zp ? ((r == 0 ? z1 : 0.0) + res[r]) : res[r];
-            }
-          }
+            for (int r = 0; r < B; ++r) st_relaxed(o + r, res[r]);
           }
           if (pos == 0 && g_wave_log && c < WAVE_LOG_CHUNKS && k - s0 < WAVE_LOG_STEPS) {
             unsigned long long tt;
@@ -449,9 +433,8 @@ static size_t wave_smem(const cprb_wave& W, int b) {
 }
 
 template <int B, bool UPPER>
-static int launch_wave(const cprb_wave& W, const double* rhs_steps, double* out_nat,
-                       double* next_rhs, const double* zp, double* final_out, int32_t* ticket,
-                       cudaStream_t st) {
+static int launch_wave(const cprb_wave& W, const double* rhs_steps, double* out_step,
+                       int32_t* ticket, cudaStream_t st) {
   static int num_sms = 0;
   if (!num_sms) {
     int dev = 0;
@@ -459,32 +442,69 @@ static int launch_wave(const cprb_wave& W, const double* rhs_steps, double* out_
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   if (W.nchunks <= 0) return CPRB_OK;
+  const int grid = W.nchunks < num_sms ? W.nchunks : num_sms;
   const size_t smem = wave_smem(W, B);
   cudaFuncSetAttribute(k_wave<B, UPPER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int grid = W.nchunks < num_sms ? W.nchunks : num_sms;
-  k_wave<B, UPPER><<<grid, WAVE_THREADS, smem, st>>>(W, rhs_steps, out_nat, next_rhs, zp,
-                                                     final_out, ticket);
+  k_wave<B, UPPER><<<grid, WAVE_THREADS, smem, st>>>(W, rhs_steps, out_step, ticket);
   return check_launch("wave solve");
 }
 
-// L then U; rhsL: r in L-step order; zl: natural z (sentinel-armed by caller);
-// zu_rhs: z in U-step order (written by L); y: natural y (sentinel-armed by
-// caller); zout = Pi zp + y.
-int wave_solve(const cprb_bilu& F, const double* rhsL, double* zl, double* zu_rhs, double* y,
-               const double* zp, double* zout, cudaStream_t st) {
+// U-plan rhs from the L solve's step-ordered output: rhs_u[u_slot[i] + c] =
+// zl_step[l_slot[i] + c] (one coalesced gather pass between the solves)
+__global__ void k_l_to_u(int n, int b, const int32_t* __restrict__ ls, const int32_t* __restrict__ us,
+                         const double* __restrict__ z, double* __restrict__ rhs_u) {
+  pdl_trigger();
+  pdl_wait();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int a = __ldg(ls + i), d = __ldg(us + i);
+    for (int c = 0; c < b; ++c) rhs_u[d + c] = z[a + c];
+  }
+}
+
+// L solve -> permute -> U solve.  rhsL: r in L-step order; F.zl_step and
+// F.y_step must be sentinel-armed; y is left in U-step order in F.y_step.
+int wave_solve(const cprb_bilu& F, const double* rhsL, cudaStream_t st) {
   int rc;
+  const int blocks = (F.n + 255) / 256 < 4 * 148 ? (F.n + 255) / 256 : 4 * 148;
   if (F.b == 3) {
-    rc = launch_wave<3, false>(F.Lw, rhsL, zl, zu_rhs, nullptr, nullptr, F.tickets + 2, st);
+    rc = launch_wave<3, false>(F.Lw, rhsL, F.zl_step, F.tickets + 2, st);
     if (rc) return rc;
-    rc = launch_wave<3, true>(F.Uw, zu_rhs, y, nullptr, zp, zout, F.tickets + 3, st);
+    launch_pdl(k_l_to_u, blocks, 256, 0, st, F.n, 3, F.l_slot, F.u_slot, (const double*)F.zl_step,
+               F.rhs_u);
+    rc = launch_wave<3, true>(F.Uw, F.rhs_u, F.y_step, F.tickets + 3, st);
   } else if (F.b == 1) {
-    rc = launch_wave<1, false>(F.Lw, rhsL, zl, zu_rhs, nullptr, nullptr, F.tickets + 2, st);
+    rc = launch_wave<1, false>(F.Lw, rhsL, F.zl_step, F.tickets + 2, st);
     if (rc) return rc;
-    rc = launch_wave<1, true>(F.Uw, zu_rhs, y, nullptr, zp, zout, F.tickets + 3, st);
+    launch_pdl(k_l_to_u, blocks, 256, 0, st, F.n, 1, F.l_slot, F.u_slot, (const double*)F.zl_step,
+               F.rhs_u);
+    rc = launch_wave<1, true>(F.Uw, F.rhs_u, F.y_step, F.tickets + 3, st);
   } else {
     return set_error(CPRB_EUNSUPPORTED, "wave BILU supports block sizes 1 and 3");
   }
   return rc;
+}
+
+// z = Pi zp + y (zp == nullptr: z = y), y gathered from U-step order
+__global__ void k_wave_combine(int n, int b, const int32_t* __restrict__ us,
+                               const double* __restrict__ y_step, const double* __restrict__ zp,
+                               double* __restrict__ z) {
+  pdl_trigger();
+  pdl_wait();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int d = __ldg(us + i);
+    for (int c = 0; c < b; ++c) {
+      const double y = y_step[d + c];
+      // src/cpr.py:184-186: prolong(zp) has zeros off the pressure slot
+      z[(int64_t)b * i + c] = zp ? ((c == 0 ? zp[i] : 0.0) + y) : y;
+    }
+  }
+}
+
+int wave_combine(const cprb_bilu& F, const double* zp, double* z, cudaStream_t st) {
+  const int blocks = (F.n + 255) / 256 < 4 * 148 ? (F.n + 255) / 256 : 4 * 148;
+  launch_pdl(k_wave_combine, blocks, 256, 0, st, F.n, F.b, F.u_slot, (const double*)F.y_step, zp,
+             z);
+  return check_launch("wave combine");
 }
 
 }  // namespace cprb

@@ -247,7 +247,10 @@ def wave_plan(T: BlockCsrMatrix, sched: LevelSchedule, b: int, upper: bool, uinv
     diff = row_step[ri] - row_step[dep]
     internal = (chunk[dep] == chunk[ri]) & (diff >= 1) & (diff <= WAVE_DINT)
     slot = (diff - 1) * WAVE_WMAX + row_pos[dep]
-    code = np.where(internal, -(slot + 1), dep)
+    # global dependencies are polled in the producer's step-ordered output
+    # (the kernel publishes rows contiguously in rhs-slot order)
+    pslot = roff[row_step] + row_pos * b
+    code = np.where(internal, -(slot + 1), pslot[dep])
     e_st = row_step[ri]
     e_rec = rec[ri]
     e_ln = ln[ri]
@@ -301,17 +304,23 @@ class DeviceBilu:
         self.use_wave = bool(F.n > 0 and use_wave)
         if self.use_wave:
             hu, uslot = wave_plan(F.U, F.u_schedule, b, True, uinv=F.u_diag_inv)
-            hl, lslot = wave_plan(F.L, F.l_schedule, b, False, aux_slot=uslot)
+            hl, lslot = wave_plan(F.L, F.l_schedule, b, False)
             self.Lw, self.Uw = WaveDev(hl), WaveDev(hu)
             self.l_slot = D.upload(lslot.astype(np.int32))
-            self.rhs_l = D.zeros(max(hl["rhs_len"], 1))
-            self.rhs_u = D.zeros(max(hu["rhs_len"], 1))
-            wl, wu, ls, rl, ru = (self.Lw.desc, self.Uw.desc, D.ptr(self.l_slot),
-                                  D.ptr(self.rhs_l), D.ptr(self.rhs_u))
+            self.u_slot = D.upload(uslot.astype(np.int32))
+            self.len_l, self.len_u = max(hl["rhs_len"], 1), max(hu["rhs_len"], 1)
+            self.rhs_l = D.zeros(self.len_l)
+            self.rhs_u = D.zeros(self.len_u)
+            self.zl_step = D.zeros(self.len_l)
+            self.y_step = D.zeros(self.len_u)
+            extra = (D.ptr(self.l_slot), D.ptr(self.rhs_l), D.ptr(self.rhs_u), D.ptr(self.u_slot),
+                     D.ptr(self.zl_step), D.ptr(self.y_step), self.len_l, self.len_u)
+            wl, wu = self.Lw.desc, self.Uw.desc
         else:
-            wl, wu, ls, rl, ru = N.Wave(), N.Wave(), 0, 0, 0
+            wl, wu = N.Wave(), N.Wave()
+            extra = (0, 0, 0, 0, 0, 0, 0, 0)
         self.desc = N.Bilu(F.n, b, self.L.desc, self.U.desc, D.ptr(self.uinv), D.ptr(self.tickets),
-                           1 if self.use_wave else 0, wl, wu, ls, rl, ru)
+                           1 if self.use_wave else 0, wl, wu, *extra)
 
     def apply(self, r, z):
         N.check(N.lib().cprb_bilu_apply(C.byref(self.desc), D.ptr(r), D.ptr(z), D.ptr(self.work),
