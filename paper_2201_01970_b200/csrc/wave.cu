@@ -46,9 +46,7 @@ constexpr int WAVE_EXPORT = 1 << 30;
 // diagnostic timeline (cprb_wave_set_log): [UPPER][chunk][local step] ->
 // %globaltimer when row position 0 of the step finished; nullptr = off
 __device__ unsigned long long* g_wave_log = nullptr;
-// diagnostic mode bits (timing experiments only; results are wrong when set):
-// 1 = do not wait on ring flags, 2 = skip global result stores, 4 = plain flag store
-__device__ int g_wave_mode = 0;
+
 constexpr int WAVE_LOG_STEPS = 512;
 constexpr int WAVE_LOG_CHUNKS = 256;
 
@@ -141,9 +139,8 @@ __device__ __forceinline__ void ring_value(const Ring& ring, int k, int q, doubl
   const int pos = q - (diff - 1) * WAVE_THREADS;
   const int dstep = k - diff;
   const uint32_t slot = (uint32_t)((dstep % WAVE_RING) * WAVE_THREADS + pos);
-  if (!(g_wave_mode & 1))
-    while (lds_acquire_s32(ring.flag + 4u * slot) != dstep) {
-    }
+  while (lds_acquire_s32(ring.flag + 4u * slot) != dstep) {
+  }
 #pragma unroll
   for (int c = 0; c < B; ++c) v[c] = lds_f64(ring.vals + 8u * (slot * B + c));
 }
@@ -262,6 +259,7 @@ __global__ void __launch_bounds__(WAVE_THREADS, 1)
     k_wave(const cprb_wave W, const double* __restrict__ rhs_steps, double* out_step,
            int32_t* ticket) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
+  unsigned long long* const tlog = g_wave_log;  // diagnostic timeline (read once)
   __shared__ StepMeta s_meta[WAVE_META];
   __shared__ __align__(8) uint64_t s_full[WAVE_NWARPS][WAVE_DEPTH];
   __shared__ int s_prog[WAVE_NWARPS];
@@ -349,9 +347,9 @@ __global__ void __launch_bounds__(WAVE_THREADS, 1)
     top_up();
     for (int k = s0; k < s1; ++k) {
       const StepMeta mk = meta(k);
-      // skew bound (see WAVE_SKEW)
-      if (k - WAVE_SKEW >= s0) {
-        const int need = k - WAVE_SKEW;
+      // skew bound (see WAVE_SKEW), checked every 4th step for the next 4
+      if (((k - s0) & 3) == 0 && k + 3 - WAVE_SKEW >= s0) {
+        const int need = k + 3 - WAVE_SKEW;
 #pragma unroll
         for (int q = 0; q < WAVE_NWARPS; ++q)
           while (lds_acquire_s32(sprog + 4u * q) < need) {
@@ -387,24 +385,19 @@ __global__ void __launch_bounds__(WAVE_THREADS, 1)
           const uint32_t slot = (uint32_t)((k % WAVE_RING) * WAVE_THREADS + pos);
 #pragma unroll
           for (int r = 0; r < B; ++r) sts_f64(ring.vals + 8u * (slot * B + r), res[r]);
-          const int mode = g_wave_mode;
-          if (mode & 4) {
-            asm volatile("st.shared.b32 [%0], %1;" ::"r"(ring.flag + 4u * slot), "r"(k) : "memory");
-          } else {
-            sts_release_s32(ring.flag + 4u * slot, k);
-          }
+          sts_release_s32(ring.flag + 4u * slot, k);
           // publish in step order: one contiguous, coalesced row block per
           // warp (the next chunk's polls, the U solve's input and the final
           // combine all read this array)
-          if (!(mode & 2)) {
+          {
             double* o = out_step + mk.rhs_off + (int64_t)pos * B;
 #pragma unroll
             for (int r = 0; r < B; ++r) st_relaxed(o + r, res[r]);
           }
-          if (pos == 0 && g_wave_log && c < WAVE_LOG_CHUNKS && k - s0 < WAVE_LOG_STEPS) {
+          if (pos == 0 && tlog && c < WAVE_LOG_CHUNKS && k - s0 < WAVE_LOG_STEPS) {
             unsigned long long tt;
             asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tt));
-            g_wave_log[((UPPER ? 1 : 0) * WAVE_LOG_CHUNKS + c) * WAVE_LOG_STEPS + (k - s0)] = tt;
+            tlog[((UPPER ? 1 : 0) * WAVE_LOG_CHUNKS + c) * WAVE_LOG_STEPS + (k - s0)] = tt;
           }
         }
         __syncwarp();
@@ -512,9 +505,7 @@ int wave_combine(const cprb_bilu& F, const double* zp, double* z, cudaStream_t s
 extern "C" int cprb_wave_set_log(uint64_t* dev_log) {
   unsigned long long* p = (unsigned long long*)dev_log;
   cudaMemcpyToSymbol(cprb::g_wave_log, &p, sizeof(p));
-  const char* m = getenv("CPRB_WAVE_DIAG_MODE");
-  int mode = (p && m) ? atoi(m) : 0;
-  cudaMemcpyToSymbol(cprb::g_wave_mode, &mode, sizeof(mode));
+
   return cprb::check_launch("wave log");
 }
 
