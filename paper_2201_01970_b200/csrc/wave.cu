@@ -406,8 +406,12 @@ __global__ void __launch_bounds__(WAVE_THREADS, 1)
           top_up();  // refill the slot just released
         }
       }
-      __syncwarp();
-      if (lane == 0) sts_release_s32(sprog + 4u * warp, k);
+      // progress is published per group of 4 steps (the skew check reads it
+      // every 4th step with a 3-step margin)
+      if (((k - s0) & 3) == 3 || k + 1 == s1) {
+        __syncwarp();
+        if (lane == 0) sts_release_s32(sprog + 4u * warp, k);
+      }
     }
   }
 }
