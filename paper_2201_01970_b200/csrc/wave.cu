@@ -353,6 +353,7 @@ __global__ void __launch_bounds__(WAVE_THREADS, 1)
 #pragma unroll
         for (int q = 0; q < WAVE_NWARPS; ++q)
           while (lds_acquire_s32(sprog + 4u * q) < need) {
+            __nanosleep(100);  // a throttled lead warp is off the critical path
           }
       }
       const int pos = warp * 32 + lane;
