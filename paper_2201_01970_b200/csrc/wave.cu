@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(WAVE_THREADS, 1)
           ++ik;
         }
       }
-      __syncwarp();
+      // no __syncwarp: the other lanes only need the mbarrier, not lane 0
     };
     top_up();
     for (int k = s0; k < s1; ++k) {
