@@ -743,6 +743,111 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) k_vtail(const TailArgs a, int
   }
 }
 
+// ---------------------------------------------------------------------------
+// Single-CTA coarse tail (k_vtail1): the same phase table, executed by one
+// 1024-thread CTA with __syncthreads between phases.  No register prefetch,
+// no cluster: for the smallest levels (a few hundred rows per colour) a
+// phase is a couple of L2 round trips instead of a dependent kernel launch.
+// ---------------------------------------------------------------------------
+constexpr int TAIL1_THREADS = 512;
+
+__device__ __forceinline__ void t1_sweep(const cprb_tail_level& L, const int32_t* ct, int k,
+                                         int flags) {
+  const int nc = L.ncolors;
+  const int s0 = ct[k], s1 = ct[k + 1];
+  const int r0 = ct[nc + 1 + k], r1 = ct[nc + 2 + k];
+  double* xout = (flags & 2) ? L.tmp : L.x;
+  const int lane = threadIdx.x & 31;
+  for (int w = s0 + (threadIdx.x >> 5); w < s1; w += TAIL1_THREADS / 32) {
+    const int row = r0 + (w - s0) * 32 + lane;
+    if (row >= r1) continue;
+    const int lid = w * 32 + lane;
+    const int len = (flags & 1) ? __ldg(L.smoother.lane_len_lo + lid) : __ldg(L.smoother.lane_len + lid);
+    const int64_t base = __ldg(L.smoother.slice_ptr + w) + lane;
+    const double d = __ldg(L.diag + row);
+    const double acc = gs_acc_from<16>(L.smoother, base, 0, len, L.x, 0.0);
+    xout[row] = (__ldcg(L.b + row) - acc) / d;
+  }
+}
+
+__global__ void __launch_bounds__(TAIL1_THREADS, 1) k_vtail1(const TailArgs a) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  constexpr int NW = TAIL1_THREADS / 32;
+  for (int p = 0; p < a.nphases; ++p) {
+    const int4 ph = __ldg(a.phases + p);
+    switch (ph.x) {
+      case TP_GATHER: {
+        const cprb_tail_level& L = a.lev[0];
+        for (int i = tid; i < L.n; i += TAIL1_THREADS) L.b[i] = a.r[(int64_t)a.stride * __ldg(a.perm0 + i)];
+        break;
+      }
+      case TP_SWEEP: {
+        const cprb_tail_level& L = a.lev[ph.y];
+        t1_sweep(L, a.colors + L.color_off, ph.z, ph.w);
+        break;
+      }
+      case TP_COPY: {
+        const cprb_tail_level& L = a.lev[ph.y];
+        const int32_t* ct = a.colors + L.color_off;
+        const int nc = L.ncolors, k = ph.z;
+        for (int i = ct[nc + 1 + k] + tid; i < ct[nc + 2 + k]; i += TAIL1_THREADS) L.x[i] = __ldcg(L.tmp + i);
+        break;
+      }
+      case TP_RR: {
+        const cprb_tail_level& L = a.lev[ph.y];
+        double* bc = (ph.y + 1 < a.nl - 1) ? a.lev[ph.y + 1].b : a.coarse_b;
+        for (int w = wid; w < L.restrict_op.nslices; w += NW) rr_slice(L.restrict_op, w, lane, L.b, L.x, bc);
+        break;
+      }
+      case TP_COARSE: {
+        for (int w = wid; w < a.n_coarse; w += NW) {
+          const double s = dense_row_dot(a.coarse_inv + (int64_t)w * a.n_coarse, a.coarse_b, a.n_coarse, lane);
+          if (lane == 0) a.coarse_x[w] = s;
+        }
+        break;
+      }
+      case TP_PROLONG: {
+        const cprb_tail_level& L = a.lev[ph.y];
+        const double* xc = (ph.y + 1 < a.nl - 1) ? a.lev[ph.y + 1].x : a.coarse_x;
+        for (int i = tid; i < L.n; i += TAIL1_THREADS) L.x[i] = __ldcg(L.x + i) + __ldcg(xc + __ldg(L.aggp + i));
+        break;
+      }
+      case TP_SCATTER: {
+        const cprb_tail_level& L = a.lev[0];
+        for (int i = tid; i < L.n; i += TAIL1_THREADS) a.z[__ldg(a.perm0 + i)] = __ldcg(L.x + i);
+        break;
+      }
+      case TP_ZERO: {
+        const cprb_tail_level& L = a.lev[ph.y];
+        for (int i = tid; i < L.n; i += TAIL1_THREADS) L.x[i] = 0.0;
+        break;
+      }
+      case TP_SEQ: {
+        if (tid == 0) {
+          const cprb_tail_level& L = a.lev[ph.y];
+          const bool bwd = ph.w & 4;
+          for (int q = 0; q < L.n; ++q) {
+            const int i = bwd ? L.n - 1 - q : q;
+            const int w = i >> 5, ln = i & 31;
+            const int len = L.smoother.lane_len[w * 32 + ln];
+            const int64_t base = L.smoother.slice_ptr[w] + ln;
+            double acc = 0.0;
+            for (int m = 0; m < len; ++m) {
+              const int64_t e = base + (int64_t)m * 32;
+              acc = acc + L.smoother.vals[e] * __ldcg(L.x + L.smoother.cols[e]);
+            }
+            L.x[i] = (__ldcg(L.b + i) - acc) / L.diag[i];
+          }
+        }
+        break;
+      }
+      default:
+        break;
+    }
+    __syncthreads();
+  }
+}
+
 static int g_tail_max = 0;
 static std::string g_tail_probe;
 
@@ -833,6 +938,10 @@ static int launch_vtail(const cprb_amg& h, const double* r, double* z, cudaStrea
   ta.stride = h.in_stride;
   ta.perm0 = h.perm0;
   ta.z = z;
+  if (g == 1 && !tlog) {  // single CTA: plain __syncthreads kernel
+    k_vtail1<<<1, TAIL1_THREADS, 0, st>>>(ta);
+    return check_launch("v-cycle tail (single CTA)");
+  }
   cudaError_t e = cudaLaunchKernelEx(&cfg, k_vtail, ta, g, tlog);
   if (e != cudaSuccess)
     return set_error(CPRB_EDEVICE, std::string("v-cycle tail launch: ") + cudaGetErrorString(e));
