@@ -115,6 +115,11 @@ def max_over_ranks(value: float, dist, torch, device: str) -> float:
     return float(t.item())
 
 
+def _config_name(grid) -> str:
+    return {(60, 220, 85): "config 3", (120, 440, 170): "config 5 on one GPU",
+            (10, 10, 10): "config 1"}.get(tuple(grid), "custom grid")
+
+
 def _grid(s):
     return tuple(int(v) for v in s.split(","))
 
@@ -262,7 +267,7 @@ def run_ours(args):
     dom = max(share, key=share.get)
     dus, dbytes = kern[dom]
     achieved = dbytes / (dus * 1e-6) / 1e9
-    traffic, traffic_src = _ncu_traffic(dom)
+    traffic, traffic_src = _ncu_traffic(dom, tuple(args.grid))
     roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
                 "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
                 "traffic": traffic, "traffic_source": traffic_src,
@@ -276,7 +281,8 @@ def run_ours(args):
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference generator restated bitwise: seed 0, drift 0.01)",
         "config": {"workload": f"SPE10-shaped {nx}x{ny}x{nz} three-phase BSR3 CPR-GMRES solve "
-                               f"(config 3), SolverConfig(theta=0, theta_amg=0, cycle='{args.cycle}')",
+                               f"({_config_name(args.grid)}), SolverConfig(theta=0, theta_amg=0, "
+                               f"cycle='{args.cycle}')",
                    "dof": n, "nnz_blocks": nnzb, "levels": len(lv),
                    "parallelism": "replicas" if ws > 1 else "single-gpu",
                    "l2": "working set > 1 GB exceeds 126 MB L2; no flush"},
@@ -298,7 +304,7 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def _ncu_traffic(kernel: str):
+def _ncu_traffic(kernel: str, grid):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`
     (a bench kernel family) from the committed ncu --set full capture
     summarised in profiles/ (tools/ncu_summary.py); None if absent."""
@@ -306,6 +312,8 @@ def _ncu_traffic(kernel: str):
     if not p.exists():
         return None, None
     d = json.loads(p.read_text())
+    if tuple(d.get("grid", (60, 220, 85))) != tuple(grid):
+        return None, None                    # captured on another workload
     e = d.get("kernels", {}).get(kernel)
     if not e:
         return None, None
@@ -410,7 +418,8 @@ def run_reference(args):
            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic (reference generator, seed 0, drift 0.01)",
            "config": {"workload": f"SPE10-shaped {nx}x{ny}x{nz} three-phase BSR3 CPR-GMRES solve "
-                                  f"(config 3), SolverConfig(theta=0, theta_amg=0, cycle='{args.cycle}')",
+                                  f"({_config_name(args.grid)}), SolverConfig(theta=0, theta_amg=0, "
+                                  f"cycle='{args.cycle}')",
                       "dof": int(b.shape[0])},
            "cpu_baseline": {"value": round(ms, 2), "unit": "ms", "cores": 1, "kind": "port",
                             "sample": sample, "host_cpus": os.cpu_count()},

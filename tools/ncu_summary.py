@@ -92,5 +92,6 @@ if lst.exists():
 (ROOT / "profiles" / f"{tag}_ncu_summary.md").write_text("\n".join(lines) + "\n")
 (ROOT / "profiles" / "ncu_traffic.json").write_text(json.dumps(
     {"source": f"profiles/{tag}_ncu_summary.md (ncu --set full, dram__bytes_read.sum + "
-               "dram__bytes_write.sum per launch group)", "kernels": traffic}, indent=1) + "\n")
+               "dram__bytes_write.sum per launch group)", "grid": [60, 220, 85], "kernels": traffic},
+    indent=1) + "\n")
 print("\n".join(lines))
