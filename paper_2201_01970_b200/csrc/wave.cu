@@ -29,9 +29,9 @@ namespace cprb {
 
 constexpr int WAVE_THREADS = 128;  // == ilu.WAVE_WMAX: rows per step == threads per CTA
 constexpr int WAVE_NWARPS = WAVE_THREADS / 32;
-constexpr int WAVE_DEPTH = 3;      // per-warp stage ring (steps in flight)
+constexpr int WAVE_DEPTH = 2;      // per-warp stage ring (steps in flight)
 constexpr int WAVE_DINT = 3;       // == ilu.WAVE_DINT: ring-served dependency distance
-constexpr int WAVE_RING = 16;      // result ring (steps)
+constexpr int WAVE_RING = 32;      // result ring (steps)
 // a warp may write step k only when every warp finished step k - SKEW, so a
 // ring slot is never overwritten while a reader of its previous occupant
 // (at most DINT steps younger) is pending
@@ -347,9 +347,9 @@ __global__ void __launch_bounds__(WAVE_THREADS, 1)
     top_up();
     for (int k = s0; k < s1; ++k) {
       const StepMeta mk = meta(k);
-      // skew bound (see WAVE_SKEW), checked every 4th step for the next 4
-      if (((k - s0) & 3) == 0 && k + 3 - WAVE_SKEW >= s0) {
-        const int need = k + 3 - WAVE_SKEW;
+      // skew bound (see WAVE_SKEW), checked every 16th step for the next 16
+      if (((k - s0) & 15) == 0 && k + 15 - WAVE_SKEW >= s0) {
+        const int need = k + 15 - WAVE_SKEW;
 #pragma unroll
         for (int q = 0; q < WAVE_NWARPS; ++q)
           while (lds_acquire_s32(sprog + 4u * q) < need) {
@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(WAVE_THREADS, 1)
       }
       // progress is published per group of 4 steps (the skew check reads it
       // every 4th step with a 3-step margin)
-      if (((k - s0) & 3) == 3 || k + 1 == s1) {
+      if (((k - s0) & 3) == 3 || k + 1 == s1) {  // (read every 16th step with margin)
         __syncwarp();
         if (lane == 0) sts_release_s32(sprog + 4u * warp, k);
       }
