@@ -165,7 +165,11 @@ typedef struct cprb_amg {
   const int32_t* tail_colors;       /* dev colour table */
   const int32_t* tail_phases;       /* dev, tail_nphases x {type, level, colour, flags} */
   int32_t tail_nphases;
-  int32_t pad_;
+  int32_t tail_mode;                /* 1: register-prefetch tail, 3: smem-resident tail */
+  const uint8_t* tail3_buf;         /* dev: per-CTA packed static data (mode 3) */
+  const int64_t* tail3_seg;         /* dev: [ctas][nphases+1] byte offsets into tail3_buf */
+  int32_t tail3_max_bytes;          /* largest per-CTA buffer (dynamic shared memory) */
+  int32_t pad2_;
 } cprb_amg;
 
 /* Chunked-wavefront plan of one triangular factor (csrc/wave.cu).  Rows are
@@ -248,6 +252,8 @@ int cprb_vtail_info(int32_t* max_ctas, char* buf, int32_t cap);
 /* Diagnostic: V-cycle kernel timeline ({kind, start, after-wait, end} u64
  * per launch, %globaltimer, <= 4096 launches); resets the counter; NULL = off. */
 int cprb_amg_set_log(uint64_t* dev_log);
+/* Diagnostic: per-phase end times of the smem-resident tail (CTA 0); NULL = off. */
+int cprb_tail3_set_log(uint64_t* dev_log);
 /* Diagnostic: run only the tail kernel, recording %globaltimer at every
  * phase boundary into dev_log (device, >= 4096 entries). */
 int cprb_vtail_timeline(const cprb_amg* h, const double* r, double* z, uint64_t* dev_log,

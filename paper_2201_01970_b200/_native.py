@@ -51,7 +51,9 @@ class Amg(C.Structure):
                 ("in_stride", C.c_int32), ("cycle", C.c_int32), ("use_fcg", C.c_int32),
                 ("kwork", vp), ("kwork_len", C.c_int64), ("tail_start", C.c_int32),
                 ("tail_ctas", C.c_int32), ("tail_levels", vp), ("tail_colors", vp),
-                ("tail_phases", vp), ("tail_nphases", C.c_int32), ("pad_", C.c_int32)]
+                ("tail_phases", vp), ("tail_nphases", C.c_int32), ("tail_mode", C.c_int32),
+                ("tail3_buf", vp), ("tail3_seg", vp), ("tail3_max_bytes", C.c_int32),
+                ("pad2_", C.c_int32)]
 
 
 class Wave(C.Structure):
@@ -94,6 +96,7 @@ _SIGS = {
     "cprb_cpr_apply": (C.c_int, [C.POINTER(Cpr), vp, vp, vp]),
     "cprb_wave_set_log": (C.c_int, [vp]),
     "cprb_amg_set_log": (C.c_int, [vp]),
+    "cprb_tail3_set_log": (C.c_int, [vp]),
     "cprb_vtail_info": (C.c_int, [i32p, C.c_char_p, C.c_int32]),
     "cprb_vtail_timeline": (C.c_int, [C.POINTER(Amg), vp, vp, vp, vp]),
     "cprb_coarse_solve": (C.c_int, [C.POINTER(Amg), vp, vp, vp]),

@@ -253,6 +253,8 @@ def _permuted_rows_sell(A, perm: np.ndarray, inv: np.ndarray):
 
 
 TAIL_ROWS = 0  # levels at most this large run in the persistent tail kernel (0 = off)
+TAIL3_CTAS = 16          # cluster size of the smem-resident tail
+TAIL3_SMEM_MAX = 200 * 1024  # per-CTA packed bytes (dynamic shared memory)
 
 
 class DeviceAmg:
@@ -382,12 +384,118 @@ class DeviceAmg:
             smooth(l, True)
         if ts == 0:
             ph.append((SCATTER, 0, 0, 0))
+        self.tail_phase_list = ph
         self.tail_phases = D.upload(np.asarray(ph, dtype=np.int32).reshape(-1))
         self.desc.tail_levels = D.ptr(self.tail_levels)
         self.desc.tail_colors = D.ptr(self.tail_colors)
         self.desc.tail_phases = D.ptr(self.tail_phases)
         self.desc.tail_nphases = len(ph)
         self.desc.tail_start = ts
+        self.desc.tail_mode = 1
+        if os.environ.get("CPRB_TAIL_MODE", "smem") == "smem":
+            packed = self._build_tail3(ts, nctas=TAIL3_CTAS)
+            if packed is not None:
+                flat, seg, maxb = packed
+                self.tail3_buf = D.upload(flat)
+                self.tail3_seg = D.upload(seg.reshape(-1))
+                self.desc.tail3_buf = D.ptr(self.tail3_buf)
+                self.desc.tail3_seg = D.ptr(self.tail3_seg)
+                self.desc.tail3_max_bytes = int(maxb)
+                self.desc.tail_mode = 3
+                self.desc.tail_ctas = TAIL3_CTAS
+
+    # -- smem-resident cluster tail (csrc/amg.cu k_vtail3) ------------------------
+    def _build_tail3(self, ts: int, nctas: int = 16):
+        """Pack the static data of levels >= ts (colour sweeps, residual +
+        restriction, prolongation maps, coarse inverse rows) into one byte
+        buffer per CTA of a `nctas` cluster, one 16-byte aligned segment per
+        phase of self.tail_phases.  Returns None if a level needs a phase the
+        smem kernel does not handle (single colour, snapshot colour, ts == 0)
+        or the largest CTA buffer exceeds shared memory."""
+        ph = np.asarray(self.tail_phase_list, dtype=np.int32)
+        GATHER, SWEEP, COPY, RR, COARSE, PROLONG, SCATTER, SEQ, ZERO = range(9)
+        if ts == 0 or np.isin(ph[:, 0], (GATHER, COPY, SCATTER, SEQ, ZERO)).any():
+            return None
+        bufs = [bytearray() for _ in range(nctas)]
+        seg = np.zeros((nctas, len(ph) + 1), dtype=np.int64)
+
+        def put(q, *arrays):
+            b = bufs[q]
+            for a in arrays:
+                raw = np.ascontiguousarray(a).tobytes()
+                b.extend(raw)
+                b.extend(b"\0" * ((-len(raw)) % 16))
+
+        def split(n):
+            m = -(-n // nctas)
+            return [(min(q * m, n), min((q + 1) * m, n)) for q in range(nctas)]
+
+        inv = self.h.coarsest_lu[1]
+        for pi, (typ, l, k, flags) in enumerate(ph):
+            for q in range(nctas):
+                seg[q, pi] = len(bufs[q])
+            if typ == SWEEP:
+                sp = self.h.levels[l].smoother.split
+                r0, r1 = int(sp.color_rows[k]), int(sp.color_rows[k + 1])
+                for q, (a, e) in enumerate(split(r1 - r0)):
+                    rows = np.arange(r0 + a, r0 + e, dtype=np.int64)
+                    cnt = rows.shape[0]
+                    lo, hi = sp.off_ptr[rows], sp.off_ptr[rows + 1]
+                    lens = hi - lo
+                    if flags & 1:   # zero-guess prefix: columns before the colour
+                        lens = np.array([int(np.searchsorted(sp.off_cols[x:y], r0)) for x, y in
+                                         zip(lo, hi)], dtype=np.int64) if cnt else lens
+                    W = int(lens.max()) if cnt else 0
+                    cols = np.zeros((W, cnt), dtype=np.int32)
+                    vals = np.zeros((W, cnt), dtype=np.float64)
+                    for t in range(cnt):
+                        L_ = int(lens[t])
+                        cols[:L_, t] = sp.off_cols[lo[t]:lo[t] + L_]
+                        vals[:L_, t] = sp.off_vals[lo[t]:lo[t] + L_]
+                    put(q, np.array([cnt, W, r0 + a, 0], dtype=np.int32), lens.astype(np.int32),
+                        sp.diag[rows].astype(np.float64), cols, vals)
+            elif typ == RR:
+                R = self.restrict[l].host
+                na = self.h.levels[l + 1].A.nrows
+                lr = R.lane_row.astype(np.int64)
+                for q, (a, e) in enumerate(split(na)):
+                    lanes = np.arange(2 * a, 2 * e, dtype=np.int64)
+                    cnt = lanes.shape[0]
+                    rows = lr[lanes]
+                    lens = np.where(rows >= 0, R.lane_len[lanes], 0).astype(np.int64)
+                    W = int(lens.max()) if cnt else 0
+                    cols = np.zeros((W, cnt), dtype=np.int32)
+                    vals = np.zeros((W, cnt), dtype=np.float64)
+                    sl, ln = lanes // 32, lanes % 32
+                    for m in range(W):
+                        ok = m < lens
+                        ent = R.slice_ptr[sl[ok]] + 32 * m + ln[ok]
+                        cols[m, ok] = R.cols[ent]
+                        vals[m, ok] = R.vals[ent]
+                    out = R.agg_out[np.arange(a, e)].astype(np.int32)
+                    put(q, np.array([cnt, W, 0, 0], dtype=np.int32), rows.astype(np.int32),
+                        lens.astype(np.int32), out, cols, vals)
+            elif typ == PROLONG:
+                aggp = self.aggp[l].cpu().numpy()
+                n = aggp.shape[0]
+                for q, (a, e) in enumerate(split(n)):
+                    put(q, np.array([e - a, 0, a, 0], dtype=np.int32), aggp[a:e])
+            elif typ == COARSE:
+                n = inv.shape[0]
+                for q, (a, e) in enumerate(split(n)):
+                    put(q, np.array([e - a, n, a, 0], dtype=np.int32),
+                        np.ascontiguousarray(inv[a:e], dtype=np.float64))
+        for q in range(nctas):
+            seg[q, len(ph)] = len(bufs[q])
+        maxb = max(len(b) for b in bufs)
+        self.tail3_bytes = maxb
+        if maxb > TAIL3_SMEM_MAX:
+            return None
+        base = np.zeros(nctas + 1, dtype=np.int64)
+        np.cumsum([len(b) for b in bufs], out=base[1:])
+        flat = np.frombuffer(b"".join(bytes(b) for b in bufs), dtype=np.uint8).copy()
+        seg = seg + base[:-1, None]          # absolute byte offsets into the flat buffer
+        return flat, seg, maxb
 
     # -- V-cycle: one native call ------------------------------------------------
     def vcycle(self, r, z):

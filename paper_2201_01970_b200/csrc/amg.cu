@@ -848,6 +848,202 @@ __global__ void __launch_bounds__(TAIL1_THREADS, 1) k_vtail1(const TailArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Shared-memory-resident cluster tail (k_vtail3).  Every CTA of a 16-CTA
+// cluster loads, once per launch, its slice of the static data of every
+// phase (packed by amg.DeviceAmg._build_tail3: row lengths, diagonal,
+// columns and values of its rows of each colour sweep, its aggregates of
+// each restriction, its prolongation map entries and coarse-inverse rows)
+// into shared memory.  A phase is then: all x gathers of a row in flight at
+// once (L2), arithmetic, one store, one cluster barrier.  Same arithmetic
+// order as the per-colour kernels (bit-identical).
+// ---------------------------------------------------------------------------
+constexpr int TAIL3_THREADS = 512;
+
+struct Tail3Args {
+  const cprb_tail_level* lev;
+  const int4* phases;
+  int nphases;
+  int nl;
+  double* coarse_b;
+  double* coarse_x;
+  const uint8_t* buf;
+  const int64_t* seg;  // [ctas][nphases + 1]
+};
+
+__device__ __forceinline__ void cluster_sync_all() {
+  __syncwarp();
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ const uint8_t* align16(const uint8_t* p) {
+  return reinterpret_cast<const uint8_t*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
+}
+
+__device__ unsigned long long* g_tail3_log = nullptr;  // diagnostic: per-phase end times (CTA 0)
+
+__global__ void __launch_bounds__(TAIL3_THREADS, 1) k_vtail3(const Tail3Args a) {
+  extern __shared__ __align__(16) uint8_t sm3[];
+  __shared__ double* s_x[32];  // per-level vector pointers (no global struct reloads
+  __shared__ double* s_b[32];  // after every cluster barrier)
+  unsigned long long* const tl = g_tail3_log;
+  if (tl && blockIdx.x == 0 && threadIdx.x == 0) tl[0] = gtimer();
+  const int q = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  constexpr int NW = TAIL3_THREADS / 32;
+  if (tid < a.nl - 1 && tid < 32) {
+    s_x[tid] = a.lev[tid].x;
+    s_b[tid] = a.lev[tid].b;
+  }
+  const int64_t* segq = a.seg + (int64_t)q * (a.nphases + 1);
+  const int64_t base = segq[0];
+  const int64_t nbytes = segq[a.nphases] - base;
+  {  // one-time load of this CTA's static data (16-byte vectors)
+    const int4* src = reinterpret_cast<const int4*>(a.buf + base);
+    int4* dst = reinterpret_cast<int4*>(sm3);
+    for (int64_t i = tid; i < nbytes / 16; i += TAIL3_THREADS) dst[i] = __ldg(src + i);
+  }
+  __syncthreads();
+  cluster_sync_all();
+  for (int p = 0; p < a.nphases; ++p) {
+    const int4 ph = __ldg(a.phases + p);
+    const uint8_t* s = sm3 + (segq[p] - base);
+    const int* hdr = reinterpret_cast<const int*>(s);
+    const int cnt = hdr[0], W = hdr[1], first = hdr[2];
+    const uint8_t* body = s + 16;
+    switch (ph.x) {
+      case TP_SWEEP: {
+        double* const Lx = s_x[ph.y];
+        const double* const Lb = s_b[ph.y];
+        const int* lens = reinterpret_cast<const int*>(body);
+        const double* diag = reinterpret_cast<const double*>(align16(body + 4 * cnt));
+        const int* cols = reinterpret_cast<const int*>(align16(reinterpret_cast<const uint8_t*>(diag + cnt)));
+        const double* vals = reinterpret_cast<const double*>(align16(reinterpret_cast<const uint8_t*>(cols + (size_t)W * cnt)));
+        for (int t = tid; t < cnt; t += TAIL3_THREADS) {
+          const int len = lens[t];
+          const int row = first + t;
+          const double bi = __ldcg(Lb + row);
+          double acc = 0.0;
+          if (len <= 32) {  // every gather of the row in flight at once
+            double xv[32];
+#pragma unroll
+            for (int u = 0; u < 32; ++u) xv[u] = (u < len) ? __ldcg(Lx + cols[(size_t)u * cnt + t]) : 0.0;
+#pragma unroll
+            for (int u = 0; u < 32; ++u)
+              if (u < len) acc = acc + vals[(size_t)u * cnt + t] * xv[u];
+          } else {
+            for (int m = 0; m < len; ++m) acc = acc + vals[(size_t)m * cnt + t] * __ldcg(Lx + cols[(size_t)m * cnt + t]);
+          }
+          Lx[row] = (bi - acc) / diag[t];
+        }
+        break;
+      }
+      case TP_RR: {
+        const double* const Lx = s_x[ph.y];
+        const double* const Lb = s_b[ph.y];
+        double* bc = (ph.y + 1 < a.nl - 1) ? s_b[ph.y + 1] : a.coarse_b;
+        const int* rows = reinterpret_cast<const int*>(body);
+        const int* lens = reinterpret_cast<const int*>(align16(body + 4 * cnt));
+        const int* outs = reinterpret_cast<const int*>(align16(reinterpret_cast<const uint8_t*>(lens + cnt)));
+        const int* cols = reinterpret_cast<const int*>(align16(reinterpret_cast<const uint8_t*>(outs + cnt / 2)));
+        const double* vals = reinterpret_cast<const double*>(align16(reinterpret_cast<const uint8_t*>(cols + (size_t)W * cnt)));
+        // lanes 2I, 2I+1 of an aggregate are adjacent threads of one warp
+        for (int t0 = 0; t0 < cnt; t0 += TAIL3_THREADS) {
+          const int t = t0 + tid;
+          double res = 0.0;
+          if (t < cnt) {
+            const int row = rows[t];
+            const int len = lens[t];
+            if (row >= 0) {
+              double tsum;
+              if (len <= 32) {
+                double e[32];
+#pragma unroll
+                for (int mm = 0; mm < 32; ++mm)
+                  e[mm] = (mm < len) ? vals[(size_t)mm * cnt + t] * __ldcg(Lx + cols[(size_t)mm * cnt + t]) : 0.0;
+                tsum = segsum_masked<32>(e, len);
+              } else {
+                auto f = [&](int mm) -> double {
+                  return vals[(size_t)mm * cnt + t] * __ldcg(Lx + cols[(size_t)mm * cnt + t]);
+                };
+                tsum = segsum_rt(f, len);
+              }
+              res = __ldcg(Lb + row) - tsum;
+            }
+          }
+          const double other = __shfl_down_sync(CPRB_FULL, res, 1);
+          if (t < cnt && (t & 1) == 0) {
+            const int out = outs[t >> 1];
+            if (out >= 0) bc[out] = (0.0 + res) + other;
+          }
+        }
+        break;
+      }
+      case TP_PROLONG: {
+        double* const Lx = s_x[ph.y];
+        const double* xc = (ph.y + 1 < a.nl - 1) ? s_x[ph.y + 1] : a.coarse_x;
+        const int* aggp = reinterpret_cast<const int*>(body);
+        for (int t = tid; t < cnt; t += TAIL3_THREADS) {
+          const int i = first + t;
+          Lx[i] = __ldcg(Lx + i) + __ldcg(xc + aggp[t]);
+        }
+        break;
+      }
+      case TP_COARSE: {
+        const double* rowsd = reinterpret_cast<const double*>(body);
+        for (int r = wid; r < cnt; r += NW) {
+          const double* row = rowsd + (size_t)r * W;
+          double sacc = 0.0;
+          for (int c = lane; c < W; c += 32) sacc = sacc + row[c] * __ldcg(a.coarse_b + c);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) sacc = sacc + __shfl_xor_sync(CPRB_FULL, sacc, o);
+          if (lane == 0) a.coarse_x[first + r] = sacc;
+        }
+        break;
+      }
+      default:
+        break;
+    }
+    cluster_sync_all();
+    if (tl && blockIdx.x == 0 && threadIdx.x == 0) tl[1 + p] = gtimer();
+  }
+}
+
+static int launch_vtail3(const cprb_amg& h, cudaStream_t st) {
+  static bool attr = false;
+  const int g = h.tail_ctas > 0 ? h.tail_ctas : 16;
+  if (!attr) {
+    cudaFuncSetAttribute(k_vtail3, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(k_vtail3, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  Tail3Args ta;
+  ta.lev = h.tail_levels;
+  ta.phases = reinterpret_cast<const int4*>(h.tail_phases);
+  ta.nphases = h.tail_nphases;
+  ta.nl = h.nlevels;
+  ta.coarse_b = h.coarse_b;
+  ta.coarse_x = h.coarse_x;
+  ta.buf = h.tail3_buf;
+  ta.seg = h.tail3_seg;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(g);
+  cfg.blockDim = dim3(TAIL3_THREADS);
+  cfg.dynamicSmemBytes = (size_t)((h.tail3_max_bytes + 15) & ~15);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = g;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_vtail3, ta);
+  if (e != cudaSuccess)
+    return set_error(CPRB_EDEVICE, std::string("v-cycle smem tail launch: ") + cudaGetErrorString(e));
+  return check_launch("v-cycle smem tail");
+}
+
 static int g_tail_max = 0;
 static std::string g_tail_probe;
 
@@ -1024,7 +1220,10 @@ int amg_vcycle(const cprb_amg& h, const double* r, double* z, cudaStream_t st) {
     launch_rr(L, L.b, L.x, bc, st, next);
     fused = next ? 1 : 0;
   }
-  if (tail) {
+  if (tail && h.tail_mode == 3 && h.tail3_buf) {
+    int rc = launch_vtail3(h, st);
+    if (rc) return rc;
+  } else if (tail) {
     int rc = launch_vtail(h, r, z, st);
     if (rc) return rc;
   } else {
@@ -1044,6 +1243,12 @@ int amg_vcycle(const cprb_amg& h, const double* r, double* z, cudaStream_t st) {
 }  // namespace cprb
 
 using namespace cprb;
+
+extern "C" int cprb_tail3_set_log(uint64_t* dev_log) {
+  unsigned long long* p = (unsigned long long*)dev_log;
+  cudaMemcpyToSymbol(cprb::g_tail3_log, &p, sizeof(p));
+  return check_launch("tail3 log");
+}
 
 extern "C" int cprb_amg_set_log(uint64_t* dev_log) {
   unsigned long long* p = (unsigned long long*)dev_log;

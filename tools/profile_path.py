@@ -65,6 +65,28 @@ def main():
         print("tail phases", len(d), "total us", (L[-1] - L[0]) / 1e3)
         print(" ".join(f"{v:.2f}" for v in d))
         return
+    if a.what == "tail3tl":
+        t = torch
+        log = t.zeros(4096, dtype=t.int64, device="cuda")
+        N.lib().cprb_tail3_set_log(D.ptr(log))
+        for rep in range(3):
+            log.zero_()
+            N.check(N.lib().cprb_amg_cycle(C.byref(Bd.amg.desc), D.ptr(bd), D.ptr(zp), D.stream()))
+            t.cuda.synchronize()
+        N.lib().cprb_tail3_set_log(None)
+        L = log.cpu().numpy()
+        L = L[L > 0]
+        print("mode", Bd.amg.desc.tail_mode, "tail_start", Bd.amg.desc.tail_start,
+              "max bytes", Bd.amg.desc.tail3_max_bytes)
+        if L.size == 0:
+            return
+        d = np.diff(L) / 1e3
+        ph = Bd.amg.tail_phase_list
+        print("tail3 phases", len(d), "total us", (L[-1] - L[0]) / 1e3, "mode", Bd.amg.desc.tail_mode)
+        print("first (load+sync)", d[0] if len(d) else None)
+        for i, (p_, v) in enumerate(zip(ph, d[1:])):
+            print(f"  {i:3d} {p_} {v:.2f}")
+        return
     if a.what == "amgtl":
         t = torch
         log = t.zeros(4 * 4096, dtype=t.int64, device="cuda")
