@@ -127,9 +127,9 @@ typedef struct cprb_amg_level {
   int32_t pad_;
 } cprb_amg_level;
 
-/* Device-resident copy of one coarse level for the persistent V-cycle tail
- * (csrc/amg.cu: k_vtail).  Colour bounds live in the tail_colors table at
- * color_off: slices[ncolors+1], rows[ncolors+1], snapshot[ncolors]. */
+/* Device pointers of one coarse level for the persistent V-cycle tail
+ * (csrc/amg.cu: k_vtail3); the tail's static data itself is packed per CTA
+ * (tail3_buf).  color_off is unused (0). */
 typedef struct cprb_tail_level {
   cprb_sell smoother;
   cprb_sell restrict_op;
@@ -162,10 +162,10 @@ typedef struct cprb_amg {
   int32_t tail_start;
   int32_t tail_ctas;                /* cluster size (1..16) */
   const cprb_tail_level* tail_levels; /* dev, nlevels-1 entries (index = level) */
-  const int32_t* tail_colors;       /* dev colour table */
+  const int32_t* tail_colors;       /* unused (0) */
   const int32_t* tail_phases;       /* dev, tail_nphases x {type, level, colour, flags} */
   int32_t tail_nphases;
-  int32_t tail_mode;                /* 1: register-prefetch tail, 3: smem-resident tail */
+  int32_t tail_mode;                /* 3: shared-memory-resident cluster tail; 0: off */
   const uint8_t* tail3_buf;         /* dev: per-CTA packed static data (mode 3) */
   const int64_t* tail3_seg;         /* dev: [ctas][nphases+1] byte offsets into tail3_buf */
   int32_t tail3_max_bytes;          /* largest per-CTA buffer (dynamic shared memory) */
@@ -246,19 +246,6 @@ int cprb_pgs_scm_pass(const cprb_amg_level* lvl, const double* b, double* x, int
 /* src/amg.py:228-267  z = amg_cycle(h, r); r strided by h->in_stride. */
 int cprb_amg_cycle(const cprb_amg* h, const double* r, double* z, void* stream);
 
-/* Cluster size the persistent V-cycle tail launches with (probed once) and
- * the probe log. */
-int cprb_vtail_info(int32_t* max_ctas, char* buf, int32_t cap);
-/* Diagnostic: V-cycle kernel timeline ({kind, start, after-wait, end} u64
- * per launch, %globaltimer, <= 4096 launches); resets the counter; NULL = off. */
-int cprb_amg_set_log(uint64_t* dev_log);
-/* Diagnostic: per-phase end times of the smem-resident tail (CTA 0); NULL = off. */
-int cprb_tail3_set_log(uint64_t* dev_log);
-/* Diagnostic: run only the tail kernel, recording %globaltimer at every
- * phase boundary into dev_log (device, >= 4096 entries). */
-int cprb_vtail_timeline(const cprb_amg* h, const double* r, double* z, uint64_t* dev_log,
-                        void* stream);
-
 /* K-cycle building blocks (the K-cycle recursion, src/amg.py:177-225,
  * :256-263, is driven by the host layer with these device steps). */
 int cprb_coarse_solve(const cprb_amg* h, const double* b, double* x, void* stream);
@@ -273,6 +260,11 @@ int cprb_bilu_apply(const cprb_bilu* F, const double* r, double* z, double* work
 /* Diagnostic: record per-step completion times of the wave solves into
  * dev_log ([2][256 chunks][512 steps] uint64, %globaltimer); NULL = off. */
 int cprb_wave_set_log(uint64_t* dev_log);
+/* Diagnostic: V-cycle kernel timeline ({kind, start, after-wait, end} u64 per
+ * launch, %globaltimer, <= 4096 launches); resets the counter; NULL = off. */
+int cprb_amg_set_log(uint64_t* dev_log);
+/* Diagnostic: per-phase end times of the smem-resident tail (CTA 0); NULL = off. */
+int cprb_tail3_set_log(uint64_t* dev_log);
 
 /* src/cpr.py:178-186  z = B r (V-cycle pressure stage). */
 int cprb_cpr_apply(const cprb_cpr* P, const double* r, double* z, void* stream);

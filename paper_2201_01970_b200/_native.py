@@ -97,8 +97,6 @@ _SIGS = {
     "cprb_wave_set_log": (C.c_int, [vp]),
     "cprb_amg_set_log": (C.c_int, [vp]),
     "cprb_tail3_set_log": (C.c_int, [vp]),
-    "cprb_vtail_info": (C.c_int, [i32p, C.c_char_p, C.c_int32]),
-    "cprb_vtail_timeline": (C.c_int, [C.POINTER(Amg), vp, vp, vp, vp]),
     "cprb_coarse_solve": (C.c_int, [C.POINTER(Amg), vp, vp, vp]),
     "cprb_resid_restrict": (C.c_int, [C.POINTER(AmgLevel), vp, vp, vp, vp]),
     "cprb_prolong": (C.c_int, [C.POINTER(AmgLevel), vp, vp, vp]),

@@ -323,98 +323,73 @@ class DeviceAmg:
         self._build_tail()
 
     def _build_tail(self):
-        """Device descriptors of the levels handled by the persistent tail
-        kernel (csrc/amg.cu k_vtail): every level with at most TAIL_ROWS rows."""
+        """Phase table and packed per-CTA static data of the levels handled by
+        the persistent cluster tail kernel (csrc/amg.cu k_vtail3): every level
+        with at most TAIL_ROWS rows (CPRB_TAIL_ROWS overrides; 0 = off)."""
         L = self.nlevels
         self.desc.tail_start = L - 1
-        self.desc.tail_ctas = int(os.environ.get("CPRB_TAIL_CTAS", "16"))
+        self.desc.tail_mode = 0
         if L <= 1:
             return
         limit = int(os.environ.get("CPRB_TAIL_ROWS", str(TAIL_ROWS)))
         ts = L - 1
-        for l in range(L - 1):
+        for l in range(1, L - 1):
             if self.h.levels[l].A.nrows <= limit:
                 ts = l
                 break
         if ts >= L - 1:
             return
         arr = (N.TailLevel * (L - 1))()
-        table = []
         for l, dl in enumerate(self.levels):
             d = dl.desc
             t = arr[l]
             t.smoother = d.smoother
             t.restrict_op = d.restrict_op
             t.diag, t.aggp, t.b, t.x, t.tmp = d.diag, d.aggp, d.b, d.x, d.tmp
-            t.n, t.ncolors, t.color_off = d.n, d.ncolors, len(table)
-            table.extend(dl.color_slices.tolist())
-            table.extend(dl.color_rows.tolist())
-            table.extend(dl.snapshot.astype(np.int32).tolist())
-        raw = np.frombuffer(bytes(arr), dtype=np.uint8).copy()
-        self.tail_levels = D.upload(raw)
-        self.tail_colors = D.upload(np.asarray(table, dtype=np.int32))
+            t.n, t.ncolors, t.color_off = d.n, d.ncolors, 0
         # phase table {type, level, colour, flags} (csrc/amg.cu TP_*): flags
-        # bit0 = zero-guess prefix, bit1 = snapshot colour (write tmp), bit2 = backward
-        GATHER, SWEEP, COPY, RR, COARSE, PROLONG, SCATTER, SEQ, ZERO = range(9)
+        # bit0 = zero-guess prefix (forward), 0 = full row (backward)
+        SWEEP, RR, COARSE, PROLONG = 1, 3, 4, 5
         ph = []
-        if ts == 0:
-            ph.append((GATHER, 0, 0, 0))
-
-        def smooth(l, backward):
-            dl = self.levels[l]
-            c = dl.desc.ncolors
-            if c == 1:
-                if not backward:
-                    ph.append((ZERO, l, 0, 0))
-                ph.append((SEQ, l, 0, 4 if backward else 0))
-                return
-            for q in range(c):
-                k = c - 1 - q if backward else q
-                snap = int(dl.snapshot[k]) if k < len(dl.snapshot) else 0
-                ph.append((SWEEP, l, k, (0 if backward else 1) | (2 * snap)))
-                if snap:
-                    ph.append((COPY, l, k, 0))
-
         for l in range(ts, L - 1):
-            smooth(l, False)
+            dl = self.levels[l]
+            if dl.desc.ncolors == 1 or dl.snapshot.any():
+                return                  # sequential GS / snapshot colours: launch path
+            ph += [(SWEEP, l, k, 1) for k in range(dl.desc.ncolors)]
             ph.append((RR, l, 0, 0))
         ph.append((COARSE, 0, 0, 0))
         for l in range(L - 2, ts - 1, -1):
             ph.append((PROLONG, l, 0, 0))
-            smooth(l, True)
-        if ts == 0:
-            ph.append((SCATTER, 0, 0, 0))
+            ph += [(SWEEP, l, k, 0) for k in range(self.levels[l].desc.ncolors - 1, -1, -1)]
         self.tail_phase_list = ph
+        packed = self._build_tail3(ts, nctas=TAIL3_CTAS)
+        if packed is None:
+            return
+        flat, seg, maxb = packed
+        self.tail_levels = D.upload(np.frombuffer(bytes(arr), dtype=np.uint8).copy())
         self.tail_phases = D.upload(np.asarray(ph, dtype=np.int32).reshape(-1))
+        self.tail3_buf = D.upload(flat)
+        self.tail3_seg = D.upload(seg.reshape(-1))
         self.desc.tail_levels = D.ptr(self.tail_levels)
-        self.desc.tail_colors = D.ptr(self.tail_colors)
         self.desc.tail_phases = D.ptr(self.tail_phases)
         self.desc.tail_nphases = len(ph)
+        self.desc.tail3_buf = D.ptr(self.tail3_buf)
+        self.desc.tail3_seg = D.ptr(self.tail3_seg)
+        self.desc.tail3_max_bytes = int(maxb)
+        self.desc.tail_ctas = TAIL3_CTAS
         self.desc.tail_start = ts
-        self.desc.tail_mode = 1
-        if os.environ.get("CPRB_TAIL_MODE", "smem") == "smem":
-            packed = self._build_tail3(ts, nctas=TAIL3_CTAS)
-            if packed is not None:
-                flat, seg, maxb = packed
-                self.tail3_buf = D.upload(flat)
-                self.tail3_seg = D.upload(seg.reshape(-1))
-                self.desc.tail3_buf = D.ptr(self.tail3_buf)
-                self.desc.tail3_seg = D.ptr(self.tail3_seg)
-                self.desc.tail3_max_bytes = int(maxb)
-                self.desc.tail_mode = 3
-                self.desc.tail_ctas = TAIL3_CTAS
+        self.desc.tail_mode = 3
 
     # -- smem-resident cluster tail (csrc/amg.cu k_vtail3) ------------------------
     def _build_tail3(self, ts: int, nctas: int = 16):
         """Pack the static data of levels >= ts (colour sweeps, residual +
         restriction, prolongation maps, coarse inverse rows) into one byte
         buffer per CTA of a `nctas` cluster, one 16-byte aligned segment per
-        phase of self.tail_phases.  Returns None if a level needs a phase the
-        smem kernel does not handle (single colour, snapshot colour, ts == 0)
-        or the largest CTA buffer exceeds shared memory."""
+        phase of self.tail_phase_list.  Returns None if the largest CTA
+        buffer exceeds shared memory."""
         ph = np.asarray(self.tail_phase_list, dtype=np.int32)
-        GATHER, SWEEP, COPY, RR, COARSE, PROLONG, SCATTER, SEQ, ZERO = range(9)
-        if ts == 0 or np.isin(ph[:, 0], (GATHER, COPY, SCATTER, SEQ, ZERO)).any():
+        SWEEP, RR, COARSE, PROLONG = 1, 3, 4, 5
+        if ts == 0:
             return None
         bufs = [bytearray() for _ in range(nctas)]
         seg = np.zeros((nctas, len(ph) + 1), dtype=np.int64)

@@ -389,463 +389,18 @@ __global__ void k_scatter(int n, const int32_t* __restrict__ idx, const double* 
 }
 
 // ---------------------------------------------------------------------------
-// Persistent V-cycle tail.  Levels >= tail_start (their colour sweeps, fused
-// residual + restriction, prolongation) and the coarse solve run in ONE
-// kernel launched as a single thread-block cluster; phases are separated by a
-// cluster barrier (~0.2 us) instead of a dependent kernel launch (~3-5 us).
-// The coarse levels are small (L2 resident after the first touch), so their
-// cost is the number of dependent phases, not bandwidth.  Same arithmetic as
-// the per-colour kernels above (bit-identical results).
+// Persistent V-cycle tail (k_vtail3 below).  Levels >= tail_start (their
+// colour sweeps, fused residual + restriction, prolongation) and the coarse
+// solve run in ONE kernel launched as a single 16-CTA thread-block cluster,
+// driven by a phase table {type, level, colour, flags} built by
+// amg.DeviceAmg._build_tail.
 // ---------------------------------------------------------------------------
-constexpr int TAIL_THREADS = 256;  // 255 registers: the next phase is held in registers
-
-struct TailCtx {
-  int gtid, nthreads, gwarp, nwarps, lane, nctas;
-  unsigned long long* tlog;  // debug timeline (CTA 0 thread 0), nullptr = off
-  int* tn;
-};
+enum { TP_SWEEP = 1, TP_RR = 3, TP_COARSE = 4, TP_PROLONG = 5 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
-}
-
-__device__ __forceinline__ void tail_sync(const TailCtx& t) {
-  if (t.tlog && t.gtid == 0) t.tlog[(*t.tn)++] = gtimer();
-  __syncwarp();
-  if (t.nctas > 1) {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-  } else {
-    __syncthreads();
-  }
-}
-
-__device__ __forceinline__ void tail_colour(const TailCtx& t, const cprb_tail_level& L,
-                                            const int32_t* ct, int k, bool zg, double* x) {
-  const int nc = L.ncolors;
-  const int s0 = ct[k], s1 = ct[k + 1];
-  const int r0 = ct[nc + 1 + k], r1 = ct[nc + 1 + k + 1];
-  const bool snap = ct[2 * (nc + 1) + k] != 0;
-  double* xout = snap ? L.tmp : x;
-  for (int w = s0 + t.gwarp; w < s1; w += t.nwarps) {
-    const int row = r0 + (w - s0) * 32 + t.lane;
-    if (row >= r1) continue;
-    const int lid = w * 32 + t.lane;
-    const int len = zg ? __ldg(L.smoother.lane_len_lo + lid) : __ldg(L.smoother.lane_len + lid);
-    const int64_t base = __ldg(L.smoother.slice_ptr + w) + t.lane;
-    const double acc = gs_acc_from<16>(L.smoother, base, 0, len, x, 0.0);
-    xout[row] = (__ldcg(L.b + row) - acc) / __ldg(L.diag + row);
-  }
-  if (snap) {
-    tail_sync(t);
-    for (int i = r0 + t.gtid; i < r1; i += t.nthreads) x[i] = __ldcg(L.tmp + i);
-  }
-  tail_sync(t);
-}
-
-__device__ __forceinline__ void tail_pass(const TailCtx& t, const cprb_tail_level& L,
-                                          const int32_t* ct, int dir, bool zg) {
-  const int c = L.ncolors;
-  if (c == 1) {  // classic sequential GS (src/smoothers.py:296-299)
-    if (zg) {
-      for (int i = t.gtid; i < L.n; i += t.nthreads) L.x[i] = 0.0;
-      tail_sync(t);
-    }
-    if (t.gtid == 0) {
-      for (int q = 0; q < L.n; ++q) {
-        const int i = dir ? L.n - 1 - q : q;
-        const int w = i >> 5, lane = i & 31;
-        const int len = L.smoother.lane_len[w * 32 + lane];
-        const int64_t base = L.smoother.slice_ptr[w] + lane;
-        double acc = 0.0;
-        for (int m = 0; m < len; ++m) {
-          const int64_t e = base + (int64_t)m * 32;
-          acc = acc + L.smoother.vals[e] * __ldcg(L.x + L.smoother.cols[e]);
-        }
-        L.x[i] = (__ldcg(L.b + i) - acc) / L.diag[i];
-      }
-    }
-    tail_sync(t);
-    return;
-  }
-  for (int q = 0; q < c; ++q) tail_colour(t, L, ct, dir ? c - 1 - q : q, zg, L.x);
-}
-
-__device__ __forceinline__ double dense_row_dot(const double* row, const double* b, int n,
-                                                int lane) {
-  double s = 0.0;
-  for (int c = lane; c < n; c += 32) s = s + __ldg(row + c) * __ldcg(b + c);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s = s + __shfl_xor_sync(CPRB_FULL, s, o);
-  return s;
-}
-
-// Phase-table driven tail (phases built by amg.DeviceAmg._build_tail):
-//   int32 [type, level, colour, flags] per phase.  Between phases every warp
-// already holds (in registers) the static data of its first work item of the
-// NEXT phase -- row lengths, slice bases, diagonal, up to TAIL_PF columns and
-// values -- so after the cluster barrier only the x gathers and b remain.
-enum { TP_GATHER = 0, TP_SWEEP = 1, TP_COPY = 2, TP_RR = 3, TP_COARSE = 4, TP_PROLONG = 5,
-       TP_SCATTER = 6, TP_SEQ = 7, TP_ZERO = 8 };
-constexpr int TAIL_PF = 16;
-
-struct TailPf {
-  int len, row, out, a;
-  int64_t base;
-  double d;
-  int col[TAIL_PF];
-  double val[TAIL_PF];
-};
-
-struct TailArgs {
-  const cprb_tail_level* lev;
-  const int32_t* colors;
-  const int4* phases;
-  int nphases;
-  int nl;
-  int n_coarse;
-  const double* coarse_inv;
-  double* coarse_b;
-  double* coarse_x;
-  const double* r;
-  int stride;
-  const int32_t* perm0;
-  double* z;
-};
-
-__device__ __forceinline__ void tail_prefetch(const TailCtx& t, const TailArgs& a, const int4 ph,
-                                              TailPf& pf) {
-  pf.len = 0;
-  pf.row = -1;
-  pf.out = -1;
-  if (ph.x == TP_SWEEP) {
-    const cprb_tail_level& L = a.lev[ph.y];
-    const int32_t* ct = a.colors + L.color_off;
-    const int nc = L.ncolors, k = ph.z;
-    const int s0 = ct[k], s1 = ct[k + 1];
-    const int r0 = ct[nc + 1 + k], r1 = ct[nc + 2 + k];
-    const int w = s0 + t.gwarp;
-    const int row = r0 + t.gwarp * 32 + t.lane;
-    if (w < s1 && row < r1) {
-      const int lid = w * 32 + t.lane;
-      pf.row = row;
-      pf.len = (ph.w & 1) ? __ldg(L.smoother.lane_len_lo + lid) : __ldg(L.smoother.lane_len + lid);
-      pf.base = __ldg(L.smoother.slice_ptr + w) + t.lane;
-      pf.d = __ldg(L.diag + row);
-#pragma unroll
-      for (int m = 0; m < TAIL_PF; ++m)
-        if (m < pf.len) {
-          pf.col[m] = __ldg(L.smoother.cols + pf.base + (int64_t)m * 32);
-          pf.val[m] = __ldg(L.smoother.vals + pf.base + (int64_t)m * 32);
-        }
-    }
-  } else if (ph.x == TP_RR) {
-    const cprb_sell& R = a.lev[ph.y].restrict_op;
-    const int w = t.gwarp;
-    if (w < R.nslices) {
-      const int lid = w * 32 + t.lane;
-      pf.row = __ldg(R.lane_row + lid);
-      pf.len = pf.row >= 0 ? __ldg(R.lane_len + lid) : 0;
-      pf.base = __ldg(R.slice_ptr + w) + t.lane;
-      pf.out = ((t.lane & 1) == 0) ? __ldg(R.agg_out + w * 16 + (t.lane >> 1)) : -1;
-#pragma unroll
-      for (int m = 0; m < TAIL_PF; ++m)
-        if (m < pf.len) {
-          pf.col[m] = __ldg(R.cols + pf.base + (int64_t)m * 32);
-          pf.val[m] = __ldg(R.vals + pf.base + (int64_t)m * 32);
-        }
-    }
-  } else if (ph.x == TP_PROLONG) {
-    const cprb_tail_level& L = a.lev[ph.y];
-    if (t.gtid < L.n) pf.a = __ldg(L.aggp + t.gtid);
-  }
-}
-
-// GS row from prefetched static data (pf) or straight from memory (first == false)
-__device__ __forceinline__ void tail_sweep_row(const cprb_tail_level& L, const double* x,
-                                               double* xout, int row, int len, int64_t base,
-                                               double d, const TailPf* pf) {
-  double acc = 0.0;
-  int m0 = 0;
-  if (pf) {
-    double xv[TAIL_PF];
-#pragma unroll
-    for (int m = 0; m < TAIL_PF; ++m) xv[m] = (m < len) ? __ldcg(x + pf->col[m]) : 0.0;
-    const double bi = __ldcg(L.b + row);
-#pragma unroll
-    for (int m = 0; m < TAIL_PF; ++m)
-      if (m < len) acc = acc + pf->val[m] * xv[m];
-    m0 = TAIL_PF;
-    if (len > m0) acc = gs_acc_from<16>(L.smoother, base, m0, len, x, acc);
-    xout[row] = (bi - acc) / d;
-    return;
-  }
-  (void)base;
-}
-
-__device__ __noinline__ void tail_sweep_rest(const TailCtx& t, const cprb_tail_level& L,
-                                             const int32_t* ct, int k, int flags) {
-  const int nc = L.ncolors;
-  const int s0 = ct[k], s1 = ct[k + 1];
-  const int r0 = ct[nc + 1 + k], r1 = ct[nc + 2 + k];
-  double* xout = (flags & 2) ? L.tmp : L.x;
-  for (int w = s0 + t.gwarp + t.nwarps; w < s1; w += t.nwarps) {
-    const int row = r0 + (w - s0) * 32 + t.lane;
-    if (row >= r1) continue;
-    const int lid = w * 32 + t.lane;
-    const int len = (flags & 1) ? __ldg(L.smoother.lane_len_lo + lid) : __ldg(L.smoother.lane_len + lid);
-    const double acc = gs_acc_from<16>(L.smoother, __ldg(L.smoother.slice_ptr + w) + t.lane, 0, len,
-                                       L.x, 0.0);
-    xout[row] = (__ldcg(L.b + row) - acc) / __ldg(L.diag + row);
-  }
-}
-
-__device__ __noinline__ void tail_rr_rest(const TailCtx& t, const cprb_sell& R, const double* b,
-                                          const double* x, double* bc) {
-  for (int w = t.gwarp + t.nwarps; w < R.nslices; w += t.nwarps) rr_slice(R, w, t.lane, b, x, bc);
-}
-
-__device__ __noinline__ double tail_rr_long(const cprb_sell& R, int64_t base, int len,
-                                            const double* x) {
-  return rr_row(R, base, 0, len, x);
-}
-
-__device__ __noinline__ void tail_coarse(const TailCtx& t, const TailArgs& a) {
-  for (int w = t.gwarp; w < a.n_coarse; w += t.nwarps) {
-    const double s = dense_row_dot(a.coarse_inv + (int64_t)w * a.n_coarse, a.coarse_b, a.n_coarse,
-                                   t.lane);
-    if (t.lane == 0) a.coarse_x[w] = s;
-  }
-}
-
-__device__ __noinline__ void tail_seq(const TailCtx& t, const cprb_tail_level& L, int backward) {
-  if (t.gtid != 0) return;
-  for (int q = 0; q < L.n; ++q) {
-    const int i = backward ? L.n - 1 - q : q;
-    const int w = i >> 5, lane = i & 31;
-    const int len = L.smoother.lane_len[w * 32 + lane];
-    const int64_t base = L.smoother.slice_ptr[w] + lane;
-    double acc = 0.0;
-    for (int m = 0; m < len; ++m) {
-      const int64_t e = base + (int64_t)m * 32;
-      acc = acc + L.smoother.vals[e] * __ldcg(L.x + L.smoother.cols[e]);
-    }
-    L.x[i] = (__ldcg(L.b + i) - acc) / L.diag[i];
-  }
-}
-
-__device__ __forceinline__ void tail_exec(const TailCtx& t, const TailArgs& a, const int4 ph,
-                                          const TailPf& pf) {
-  switch (ph.x) {
-    case TP_GATHER: {
-      const cprb_tail_level& L = a.lev[0];
-      for (int i = t.gtid; i < L.n; i += t.nthreads)
-        L.b[i] = a.r[(int64_t)a.stride * __ldg(a.perm0 + i)];
-      break;
-    }
-    case TP_SWEEP: {
-      const cprb_tail_level& L = a.lev[ph.y];
-      const int32_t* ct = a.colors + L.color_off;
-      const int nc = L.ncolors, k = ph.z;
-      const int s0 = ct[k], s1 = ct[k + 1];
-      const int r0 = ct[nc + 1 + k], r1 = ct[nc + 2 + k];
-      double* xout = (ph.w & 2) ? L.tmp : L.x;
-      if (pf.row >= 0) tail_sweep_row(L, L.x, xout, pf.row, pf.len, pf.base, pf.d, &pf);
-      if (s1 - s0 > t.nwarps) tail_sweep_rest(t, L, ct, k, ph.w);
-      (void)r0;
-      (void)r1;
-      break;
-    }
-    case TP_COPY: {
-      const cprb_tail_level& L = a.lev[ph.y];
-      const int32_t* ct = a.colors + L.color_off;
-      const int nc = L.ncolors, k = ph.z;
-      for (int i = ct[nc + 1 + k] + t.gtid; i < ct[nc + 2 + k]; i += t.nthreads) L.x[i] = __ldcg(L.tmp + i);
-      break;
-    }
-    case TP_RR: {
-      const cprb_tail_level& L = a.lev[ph.y];
-      const cprb_sell& R = L.restrict_op;
-      double* bc = (ph.y + 1 < a.nl - 1) ? a.lev[ph.y + 1].b : a.coarse_b;
-      if (t.gwarp < R.nslices) {
-        double res = 0.0;
-        if (pf.row >= 0) {
-          double t2;
-          if (pf.len <= TAIL_PF) {
-            double e[TAIL_PF];
-#pragma unroll
-            for (int m = 0; m < TAIL_PF; ++m) e[m] = (m < pf.len) ? pf.val[m] * __ldcg(L.x + pf.col[m]) : 0.0;
-            t2 = segsum_masked<TAIL_PF>(e, pf.len);
-          } else {
-            t2 = tail_rr_long(R, pf.base, pf.len, L.x);
-          }
-          res = __ldcg(L.b + pf.row) - t2;
-        }
-        const double other = __shfl_down_sync(CPRB_FULL, res, 1);
-        if ((t.lane & 1) == 0 && pf.out >= 0) bc[pf.out] = (0.0 + res) + other;
-      }
-      if (R.nslices > t.nwarps) tail_rr_rest(t, R, L.b, L.x, bc);
-      break;
-    }
-    case TP_COARSE:
-      tail_coarse(t, a);
-      break;
-    case TP_PROLONG: {
-      const cprb_tail_level& L = a.lev[ph.y];
-      const double* xc = (ph.y + 1 < a.nl - 1) ? a.lev[ph.y + 1].x : a.coarse_x;
-      if (t.gtid < L.n) L.x[t.gtid] = __ldcg(L.x + t.gtid) + __ldcg(xc + pf.a);
-      for (int i = t.gtid + t.nthreads; i < L.n; i += t.nthreads)
-        L.x[i] = __ldcg(L.x + i) + __ldcg(xc + __ldg(L.aggp + i));
-      break;
-    }
-    case TP_SCATTER: {
-      const cprb_tail_level& L = a.lev[0];
-      for (int i = t.gtid; i < L.n; i += t.nthreads) a.z[__ldg(a.perm0 + i)] = __ldcg(L.x + i);
-      break;
-    }
-    case TP_ZERO: {
-      const cprb_tail_level& L = a.lev[ph.y];
-      for (int i = t.gtid; i < L.n; i += t.nthreads) L.x[i] = 0.0;
-      break;
-    }
-    case TP_SEQ:  // single-colour level: classic sequential GS (src/smoothers.py:296-299)
-      tail_seq(t, a.lev[ph.y], ph.w & 4);
-      break;
-    default:
-      break;
-  }
-}
-
-__global__ void __launch_bounds__(TAIL_THREADS, 1) k_vtail(const TailArgs a, int nctas,
-                                                            unsigned long long* tlog) {
-  TailCtx t;
-  int tn = 0;
-  t.tlog = tlog;
-  t.tn = &tn;
-  t.nctas = nctas;
-  t.gtid = blockIdx.x * blockDim.x + threadIdx.x;
-  t.nthreads = gridDim.x * blockDim.x;
-  t.gwarp = t.gtid >> 5;
-  t.nwarps = t.nthreads >> 5;
-  t.lane = threadIdx.x & 31;
-  if (tlog && t.gtid == 0) tlog[tn++] = gtimer();
-  TailPf pf;
-  int4 ph = a.nphases > 0 ? __ldg(a.phases) : make_int4(-1, 0, 0, 0);
-  tail_prefetch(t, a, ph, pf);
-  for (int p = 0; p < a.nphases; ++p) {
-    tail_exec(t, a, ph, pf);
-    if (p + 1 < a.nphases) {
-      ph = __ldg(a.phases + p + 1);
-      tail_prefetch(t, a, ph, pf);  // static loads stay in flight across the barrier
-      tail_sync(t);
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Single-CTA coarse tail (k_vtail1): the same phase table, executed by one
-// 1024-thread CTA with __syncthreads between phases.  No register prefetch,
-// no cluster: for the smallest levels (a few hundred rows per colour) a
-// phase is a couple of L2 round trips instead of a dependent kernel launch.
-// ---------------------------------------------------------------------------
-constexpr int TAIL1_THREADS = 512;
-
-__device__ __forceinline__ void t1_sweep(const cprb_tail_level& L, const int32_t* ct, int k,
-                                         int flags) {
-  const int nc = L.ncolors;
-  const int s0 = ct[k], s1 = ct[k + 1];
-  const int r0 = ct[nc + 1 + k], r1 = ct[nc + 2 + k];
-  double* xout = (flags & 2) ? L.tmp : L.x;
-  const int lane = threadIdx.x & 31;
-  for (int w = s0 + (threadIdx.x >> 5); w < s1; w += TAIL1_THREADS / 32) {
-    const int row = r0 + (w - s0) * 32 + lane;
-    if (row >= r1) continue;
-    const int lid = w * 32 + lane;
-    const int len = (flags & 1) ? __ldg(L.smoother.lane_len_lo + lid) : __ldg(L.smoother.lane_len + lid);
-    const int64_t base = __ldg(L.smoother.slice_ptr + w) + lane;
-    const double d = __ldg(L.diag + row);
-    const double acc = gs_acc_from<16>(L.smoother, base, 0, len, L.x, 0.0);
-    xout[row] = (__ldcg(L.b + row) - acc) / d;
-  }
-}
-
-__global__ void __launch_bounds__(TAIL1_THREADS, 1) k_vtail1(const TailArgs a) {
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  constexpr int NW = TAIL1_THREADS / 32;
-  for (int p = 0; p < a.nphases; ++p) {
-    const int4 ph = __ldg(a.phases + p);
-    switch (ph.x) {
-      case TP_GATHER: {
-        const cprb_tail_level& L = a.lev[0];
-        for (int i = tid; i < L.n; i += TAIL1_THREADS) L.b[i] = a.r[(int64_t)a.stride * __ldg(a.perm0 + i)];
-        break;
-      }
-      case TP_SWEEP: {
-        const cprb_tail_level& L = a.lev[ph.y];
-        t1_sweep(L, a.colors + L.color_off, ph.z, ph.w);
-        break;
-      }
-      case TP_COPY: {
-        const cprb_tail_level& L = a.lev[ph.y];
-        const int32_t* ct = a.colors + L.color_off;
-        const int nc = L.ncolors, k = ph.z;
-        for (int i = ct[nc + 1 + k] + tid; i < ct[nc + 2 + k]; i += TAIL1_THREADS) L.x[i] = __ldcg(L.tmp + i);
-        break;
-      }
-      case TP_RR: {
-        const cprb_tail_level& L = a.lev[ph.y];
-        double* bc = (ph.y + 1 < a.nl - 1) ? a.lev[ph.y + 1].b : a.coarse_b;
-        for (int w = wid; w < L.restrict_op.nslices; w += NW) rr_slice(L.restrict_op, w, lane, L.b, L.x, bc);
-        break;
-      }
-      case TP_COARSE: {
-        for (int w = wid; w < a.n_coarse; w += NW) {
-          const double s = dense_row_dot(a.coarse_inv + (int64_t)w * a.n_coarse, a.coarse_b, a.n_coarse, lane);
-          if (lane == 0) a.coarse_x[w] = s;
-        }
-        break;
-      }
-      case TP_PROLONG: {
-        const cprb_tail_level& L = a.lev[ph.y];
-        const double* xc = (ph.y + 1 < a.nl - 1) ? a.lev[ph.y + 1].x : a.coarse_x;
-        for (int i = tid; i < L.n; i += TAIL1_THREADS) L.x[i] = __ldcg(L.x + i) + __ldcg(xc + __ldg(L.aggp + i));
-        break;
-      }
-      case TP_SCATTER: {
-        const cprb_tail_level& L = a.lev[0];
-        for (int i = tid; i < L.n; i += TAIL1_THREADS) a.z[__ldg(a.perm0 + i)] = __ldcg(L.x + i);
-        break;
-      }
-      case TP_ZERO: {
-        const cprb_tail_level& L = a.lev[ph.y];
-        for (int i = tid; i < L.n; i += TAIL1_THREADS) L.x[i] = 0.0;
-        break;
-      }
-      case TP_SEQ: {
-        if (tid == 0) {
-          const cprb_tail_level& L = a.lev[ph.y];
-          const bool bwd = ph.w & 4;
-          for (int q = 0; q < L.n; ++q) {
-            const int i = bwd ? L.n - 1 - q : q;
-            const int w = i >> 5, ln = i & 31;
-            const int len = L.smoother.lane_len[w * 32 + ln];
-            const int64_t base = L.smoother.slice_ptr[w] + ln;
-            double acc = 0.0;
-            for (int m = 0; m < len; ++m) {
-              const int64_t e = base + (int64_t)m * 32;
-              acc = acc + L.smoother.vals[e] * __ldcg(L.x + L.smoother.cols[e]);
-            }
-            L.x[i] = (__ldcg(L.b + i) - acc) / L.diag[i];
-          }
-        }
-        break;
-      }
-      default:
-        break;
-    }
-    __syncthreads();
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1044,106 +599,6 @@ static int launch_vtail3(const cprb_amg& h, cudaStream_t st) {
   return check_launch("v-cycle smem tail");
 }
 
-static int g_tail_max = 0;
-static std::string g_tail_probe;
-
-static void probe_vtail() {
-  static bool probed = false;
-  if (probed) return;
-  probed = true;
-  cudaError_t e0 = cudaFuncSetAttribute(k_vtail, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  if (e0 != cudaSuccess) {
-    g_tail_probe += std::string("nonportable attr: ") + cudaGetErrorString(e0) + "; ";
-    cudaGetLastError();
-  }
-  for (int want : {16, 8, 4, 2}) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(want);
-    cfg.blockDim = dim3(TAIL_THREADS);
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = want;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    int nclus = 0;
-    cudaError_t e = cudaOccupancyMaxActiveClusters(&nclus, k_vtail, &cfg);
-    g_tail_probe += std::to_string(want) + ":" + (e == cudaSuccess ? std::to_string(nclus) : cudaGetErrorString(e)) + " ";
-    cudaGetLastError();
-    if (e == cudaSuccess && nclus > 0) {
-      g_tail_max = want;
-      return;
-    }
-  }
-  g_tail_max = 1;
-}
-
-static int launch_vtail(const cprb_amg& h, const double* r, double* z, cudaStream_t st,
-                        unsigned long long* tlog = nullptr) {
-  static int max_ctas[2] = {0, 0};
-  static bool probed = true;
-  probe_vtail();
-  max_ctas[1] = g_tail_max;
-  if (!probed) {
-    for (int want : {16, 8, 4, 2}) {
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(want);
-      cfg.blockDim = dim3(TAIL_THREADS);
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = want;
-      at[0].val.clusterDim.y = 1;
-      at[0].val.clusterDim.z = 1;
-      cfg.attrs = at;
-      cfg.numAttrs = 1;
-      int nclus = 0;
-      if (cudaOccupancyMaxActiveClusters(&nclus, k_vtail, &cfg) == cudaSuccess && nclus > 0) {
-        max_ctas[1] = want;
-        break;
-      }
-      cudaGetLastError();
-    }
-    probed = true;
-  }
-  int g = h.tail_ctas > 0 ? h.tail_ctas : 16;
-  if (g > max_ctas[1]) g = max_ctas[1];
-  if (g < 1) g = 1;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(g);
-  cfg.blockDim = dim3(TAIL_THREADS);
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = g;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  TailArgs ta;
-  ta.lev = h.tail_levels;
-  ta.colors = h.tail_colors;
-  ta.phases = reinterpret_cast<const int4*>(h.tail_phases);
-  ta.nphases = h.tail_nphases;
-  ta.nl = h.nlevels;
-  ta.n_coarse = h.n_coarse;
-  ta.coarse_inv = h.coarse_inv;
-  ta.coarse_b = h.coarse_b;
-  ta.coarse_x = h.coarse_x;
-  ta.r = r;
-  ta.stride = h.in_stride;
-  ta.perm0 = h.perm0;
-  ta.z = z;
-  if (g == 1 && !tlog) {  // single CTA: plain __syncthreads kernel
-    k_vtail1<<<1, TAIL1_THREADS, 0, st>>>(ta);
-    return check_launch("v-cycle tail (single CTA)");
-  }
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k_vtail, ta, g, tlog);
-  if (e != cudaSuccess)
-    return set_error(CPRB_EDEVICE, std::string("v-cycle tail launch: ") + cudaGetErrorString(e));
-  return check_launch("v-cycle tail");
-}
-
 template <int ZG, int G, int SC>
 static void launch_sweep(const cprb_amg_level& L, int k, double* b, const double* gsrc,
                          int gstride, const int32_t* perm, const double* xin, double* xout,
@@ -1206,8 +661,8 @@ int amg_vcycle(const cprb_amg& h, const double* r, double* z, cudaStream_t st) {
                                                                      h.coarse_b, z, nullptr);
     return check_launch("coarse-only cycle");
   }
-  const bool tail = h.tail_levels && h.tail_colors && h.tail_phases && h.tail_nphases > 0 &&
-                    h.tail_start >= 0 && h.tail_start < nl - 1;
+  const bool tail = h.tail_mode == 3 && h.tail3_buf && h.tail_levels && h.tail_phases &&
+                    h.tail_nphases > 0 && h.tail_start >= 1 && h.tail_start < nl - 1;
   const int ts = tail ? h.tail_start : nl - 1;
   int fused = 0;  // colour 0 of this level was computed by the previous restriction
   for (int l = 0; l < ts; ++l) {
@@ -1220,11 +675,8 @@ int amg_vcycle(const cprb_amg& h, const double* r, double* z, cudaStream_t st) {
     launch_rr(L, L.b, L.x, bc, st, next);
     fused = next ? 1 : 0;
   }
-  if (tail && h.tail_mode == 3 && h.tail3_buf) {
+  if (tail) {
     int rc = launch_vtail3(h, st);
-    if (rc) return rc;
-  } else if (tail) {
-    int rc = launch_vtail(h, r, z, st);
     if (rc) return rc;
   } else {
     launch_pdl(k_dense_mv, nblk((int64_t)h.n_coarse * 32, 256), 256, 0, st, h.n_coarse,
@@ -1256,20 +708,6 @@ extern "C" int cprb_amg_set_log(uint64_t* dev_log) {
   cudaMemcpyToSymbol(cprb::g_amg_log, &p, sizeof(p));
   cudaMemcpyToSymbol(cprb::g_amg_log_n, &zero, sizeof(zero));
   return check_launch("amg log");
-}
-
-extern "C" int cprb_vtail_timeline(const cprb_amg* h, const double* r, double* z,
-                                   uint64_t* dev_log, void* stream) {
-  return launch_vtail(*h, r, z, (cudaStream_t)stream, (unsigned long long*)dev_log);
-}
-
-extern "C" int cprb_vtail_info(int32_t* max_ctas, char* buf, int32_t cap) {
-  probe_vtail();
-  *max_ctas = g_tail_max;
-  if (buf && cap > 0) {
-    std::snprintf(buf, cap, "%s", g_tail_probe.c_str());
-  }
-  return CPRB_OK;
 }
 
 extern "C" int cprb_pgs_scm_pass(const cprb_amg_level* lvl, const double* b, double* x,

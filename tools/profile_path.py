@@ -48,23 +48,6 @@ def main():
     }
     import ctypes as C
     from paper_2201_01970_b200 import _native as N
-    mx = C.c_int32(0)
-    buf = C.create_string_buffer(512)
-    N.lib().cprb_vtail_info(C.byref(mx), buf, 512)
-    print("vtail cluster:", mx.value, buf.value.decode(), "tail_start", Bd.amg.desc.tail_start)
-    if a.what == "tailtl":
-        t = torch
-        log = t.zeros(4096, dtype=t.int64, device="cuda")
-        for rep in range(3):
-            log.zero_()
-            N.lib().cprb_vtail_timeline(C.byref(Bd.amg.desc), D.ptr(bd), D.ptr(zp), D.ptr(log), D.stream())
-            t.cuda.synchronize()
-        L = log.cpu().numpy()
-        L = L[L > 0]
-        d = np.diff(L) / 1e3
-        print("tail phases", len(d), "total us", (L[-1] - L[0]) / 1e3)
-        print(" ".join(f"{v:.2f}" for v in d))
-        return
     if a.what == "tail3tl":
         t = torch
         log = t.zeros(4096, dtype=t.int64, device="cuda")
