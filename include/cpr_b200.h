@@ -300,6 +300,39 @@ int cprb_div_host(int64_t n, const double* x, double h, double* out, void* strea
 /* out = x / (*h_dev)  (src/cpr.py:262 V[0] = r / beta) */
 int cprb_div_scalar(int64_t n, const double* x, const double* h_dev, double* out, void* stream);
 
+/* ---- slab-partitioned solve (paper_2201_01970_b200/partition.py) ----
+ * Each rank owns a contiguous range of block rows; operators read a column
+ * window whose halo the host exchanges (NCCL over NVLink). */
+/* src/cpr.py:185  r2 = r - A (Pi zp) (block column 0 only; zp one value per block column). */
+int cprb_stage2_residual(const cprb_sell* A, int32_t b, const double* zp, const double* r,
+                         double* r2, void* stream);
+/* One colour of src/smoothers.py:273-318 (halo exchanged by the caller between colours). */
+int cprb_pgs_scm_color(const cprb_amg_level* lvl, int32_t k, double* b, double* x,
+                       int32_t zero_guess, const double* gsrc, int32_t gstride,
+                       const int32_t* perm, double* sout, void* stream);
+/* GPU-count-invariant reductions (src/sparse.py:361-369, src/cpr.py:276-284):
+ * per fixed global segment of seg_len entries one partial of (w, vdot)
+ * ((w, w) if vdot == NULL), after an optional MGS update w -= (*hprev) vprev;
+ * then the fixed-order sum of nseg partials (map: global segment -> slot,
+ * NULL = identity), square-rooted if sqrt_. */
+int cprb_seg_partials(int64_t n, int64_t seg_len, double* w, const double* vprev,
+                      const double* hprev, const double* vdot, double* partials, void* stream);
+int cprb_seg_finish(int32_t nseg, const double* partials, const int32_t* map, double* out,
+                    int32_t sqrt_, void* stream);
+/* w /= *h unless *h == 0 (src/cpr.py:281-284). */
+int cprb_div_if_nonzero(int64_t n, double* w, const double* h, void* stream);
+/* dst[idx[i]] += src[i]  (cross-slab aggregates of np.bincount, src/amg.py:254-255). */
+int cprb_scatter_add(int64_t n, const int32_t* idx, const double* src, double* dst, void* stream);
+/* dst[i] = src[stride * idx[i]]  (halo packing; idx NULL = identity). */
+int cprb_gather(int64_t n, const int32_t* idx, const double* src, int32_t stride, double* dst,
+                void* stream);
+/* padded all-gather [nranks][cap] -> packed; offs: device int64[nranks + 1]. */
+int cprb_unpad(int32_t nranks, int64_t cap, const int64_t* offs, const double* src, double* dst,
+               void* stream);
+/* src/cpr.py:184-186  z = Pi zp + y  for ncells block rows of size b. */
+int cprb_cpr_combine(int64_t ncells, int32_t b, const double* zp, const double* y, double* z,
+                     void* stream);
+
 #ifdef __cplusplus
 }
 #endif

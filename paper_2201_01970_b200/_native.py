@@ -95,6 +95,15 @@ _SIGS = {
     "cprb_bilu_apply": (C.c_int, [C.POINTER(Bilu), vp, vp, vp, vp]),
     "cprb_cpr_apply": (C.c_int, [C.POINTER(Cpr), vp, vp, vp]),
     "cprb_wave_set_log": (C.c_int, [vp]),
+    "cprb_stage2_residual": (C.c_int, [vp, C.c_int32, vp, vp, vp, vp]),
+    "cprb_pgs_scm_color": (C.c_int, [vp, C.c_int32, vp, vp, C.c_int32, vp, C.c_int32, vp, vp, vp]),
+    "cprb_seg_partials": (C.c_int, [C.c_int64, C.c_int64, vp, vp, vp, vp, vp, vp]),
+    "cprb_seg_finish": (C.c_int, [C.c_int32, vp, vp, vp, C.c_int32, vp]),
+    "cprb_div_if_nonzero": (C.c_int, [C.c_int64, vp, vp, vp]),
+    "cprb_scatter_add": (C.c_int, [C.c_int64, vp, vp, vp, vp]),
+    "cprb_gather": (C.c_int, [C.c_int64, vp, vp, C.c_int32, vp, vp]),
+    "cprb_unpad": (C.c_int, [C.c_int32, C.c_int64, vp, vp, vp, vp]),
+    "cprb_cpr_combine": (C.c_int, [C.c_int64, C.c_int32, vp, vp, vp, vp]),
     "cprb_amg_set_log": (C.c_int, [vp]),
     "cprb_tail3_set_log": (C.c_int, [vp]),
     "cprb_coarse_solve": (C.c_int, [C.POINTER(Amg), vp, vp, vp]),

@@ -716,6 +716,30 @@ extern "C" int cprb_pgs_scm_pass(const cprb_amg_level* lvl, const double* b, dou
                   (cudaStream_t)stream);
 }
 
+// one colour of a PGS-SCM pass (slab-partitioned path: the host exchanges
+// halo values between colours); no snapshot colours (theta_amg = 0 levels)
+extern "C" int cprb_pgs_scm_color(const cprb_amg_level* lvl, int32_t k, double* b, double* x,
+                                  int32_t zero_guess, const double* gsrc, int32_t gstride,
+                                  const int32_t* perm, double* sout, void* stream) {
+  const cprb_amg_level& L = *lvl;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (k < 0 || k >= L.ncolors) return set_error(CPRB_EINVAL, "colour index out of range");
+  if (L.color_snapshot && L.color_snapshot[k])
+    return set_error(CPRB_EUNSUPPORTED, "snapshot colours are not supported per colour");
+  const int code = (zero_guess ? 4 : 0) + (gsrc ? 2 : 0) + (sout ? 1 : 0);
+  switch (code) {
+    case 0: launch_sweep<0, 0, 0>(L, k, b, gsrc, gstride, perm, x, x, sout, st); break;
+    case 1: launch_sweep<0, 0, 1>(L, k, b, gsrc, gstride, perm, x, x, sout, st); break;
+    case 2: launch_sweep<0, 1, 0>(L, k, b, gsrc, gstride, perm, x, x, sout, st); break;
+    case 3: launch_sweep<0, 1, 1>(L, k, b, gsrc, gstride, perm, x, x, sout, st); break;
+    case 4: launch_sweep<1, 0, 0>(L, k, b, gsrc, gstride, perm, x, x, sout, st); break;
+    case 5: launch_sweep<1, 0, 1>(L, k, b, gsrc, gstride, perm, x, x, sout, st); break;
+    case 6: launch_sweep<1, 1, 0>(L, k, b, gsrc, gstride, perm, x, x, sout, st); break;
+    default: launch_sweep<1, 1, 1>(L, k, b, gsrc, gstride, perm, x, x, sout, st); break;
+  }
+  return check_launch("pgs colour");
+}
+
 extern "C" int cprb_coarse_solve(const cprb_amg* h, const double* b, double* x, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   k_dense_mv<<<nblk((int64_t)h->n_coarse * 32, 256), 256, 0, st>>>(h->n_coarse, h->coarse_inv, b, x,

@@ -145,3 +145,10 @@ extern "C" int cprb_residual(const cprb_sell* A, int32_t b, const double* rhs, c
                              double* r, int32_t* flag, void* stream) {
   return bsr_op(1, *A, b, x, rhs, r, flag, nullptr, (cudaStream_t)stream);
 }
+
+// src/cpr.py:185  r2 = r - A (Pi zp), reading only block column 0 (zp holds
+// the pressure values, one per block column)
+extern "C" int cprb_stage2_residual(const cprb_sell* A, int32_t b, const double* zp,
+                                    const double* r, double* r2, void* stream) {
+  return bsr_op(2, *A, b, zp, r, r2, nullptr, nullptr, (cudaStream_t)stream);
+}
