@@ -13,6 +13,9 @@ is the same solve through the public API from pinned host buffers.
 `--impl reference` times the CPU oracle (oracle/cprkit_oracle.py, a numpy
 restatement of the reference) on the host cores.  For N > 1 every rank solves
 its own system (seed = rank; weak scaling, no data-path collective).
+`--partition` instead row-partitions ONE system over the N ranks (strong
+scaling; NCCL halo exchange and GPU-count-invariant reductions, DESIGN.md
+section 7).
 """
 
 from __future__ import annotations
@@ -307,6 +310,102 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_partitioned(args):
+    """Row-slab partitioned solve of ONE system across the N ranks (SURVEY.md
+    8(e); paper_2201_01970_b200/partition.py): strong scaling, NCCL halos +
+    segment all-gathers, levels >= 1 on rank 0, BILU replicated."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2201_01970_b200 as P
+    from paper_2201_01970_b200 import partition as S
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    nx, ny, nz = args.grid
+    t0 = time.perf_counter()
+    (A, b), = P.generate_blackoil_like_sequence(nx, ny, nz, 1, 0.01, 0).systems
+    t_gen = time.perf_counter() - t0
+    cfg = P.SolverConfig(theta=0.0, theta_amg=0.0, cycle=args.cycle)
+    t0 = time.perf_counter()
+    B = P.build_cpr(A, cfg)
+    comm = S.SlabComm()
+    part = S.SlabPartition(A.nrows, ws)
+    cpr = S.SlabCpr(B, part, comm)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t0
+    a, e = part.rows(rank)
+    b_loc = np.ascontiguousarray(b[3 * a:3 * e])
+    bd = torch.from_numpy(b_loc).cuda()
+    params = cfg.gmres_params()
+
+    def solve(rhs):
+        return S.gmres_solve_slab(A, rhs, None, B, params, comm=comm, part=part, cpr=cpr)
+
+    for _ in range(args.warmup):
+        res = solve(bd)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    st = torch.cuda.current_stream()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        e0.record(st)
+        for _ in range(args.steps):
+            res = solve(bd)
+        e1.record(st)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    if ws > 1:
+        ms = max_over_ranks(ms, dist, torch, "cuda")
+    x = S.gather_rows(res.x, part, comm, 3).cpu().numpy()
+    xs = P.problems.manufactured_solution(nx * ny * nz)
+    x_err = float(np.linalg.norm(x - xs) / np.linalg.norm(xs))
+    b_pin = torch.from_numpy(b_loc).pin_memory()
+    te = []
+    for _ in range(max(1, min(args.steps, 3))):
+        if ws > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        r2 = solve(b_pin)
+        _ = r2.x.numpy()
+        te.append(time.perf_counter() - t0)
+    e2e_ms = float(np.median(te) * 1e3)
+    if ws > 1:
+        e2e_ms = max_over_ranks(e2e_ms, dist, torch, "cuda")
+    launches_per_solve, kernel_names = _count_launches(lambda: solve(bd), torch)
+    out = {
+        "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generator restated bitwise: seed 0, drift 0.01)",
+        "config": {"workload": f"SPE10-shaped {nx}x{ny}x{nz} three-phase BSR3 CPR-GMRES solve "
+                               f"({_config_name(args.grid)}), SolverConfig(theta=0, theta_amg=0, "
+                               f"cycle='{args.cycle}')",
+                   "dof": int(b.shape[0]), "nnz_blocks": int(A.nnz),
+                   "parallelism": f"slab-partitioned over {ws} rank(s): NCCL halos + segment "
+                                  "all-gathers; AMG levels >= 1 on rank 0; BILU replicated",
+                   "seg_cells": part.seg_cells,
+                   "l2": "working set > 1 GB exceeds 126 MB L2; no flush"},
+        "iters": {"outer": res.outer, "inner": res.inner, "rel_residual": res.rel_residual,
+                  "x_err_vs_manufactured": x_err},
+        "e2e": {"value": round(e2e_ms, 4), "unit": "ms", "h2d_bytes_per_step": int(8 * b_loc.size),
+                "d2h_bytes_per_step": int(8 * b_loc.size)},
+        "setup_s": round(t_setup, 2), "generate_s": round(t_gen, 2),
+        "gpu_launches": launches_per_solve * args.steps,
+        "gpu_launches_per_solve": launches_per_solve, "kernel_families": kernel_names,
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(out))
+    if ws > 1:
+        dist.destroy_process_group()
+
+
 def _ncu_traffic(kernel: str, grid):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`
     (a bench kernel family) from the committed ncu --set full capture
@@ -440,9 +539,13 @@ def main():
     ap.add_argument("--grid", type=_grid, default=(60, 220, 85))
     ap.add_argument("--cycle", default="v", choices=["v", "k"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--partition", action="store_true",
+                    help="row-slab partition ONE system over the N ranks (strong scaling)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.partition:
+        run_partitioned(args)
     else:
         run_ours(args)
 

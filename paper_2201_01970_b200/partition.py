@@ -128,6 +128,11 @@ class SlabComm:
             self.rank = dist.get_rank(group)
             self.size = dist.get_world_size(group)
             self.nccl = dist.get_backend(group) == "nccl"
+            if self.nccl and self.size > 1:
+                # every rank joins one collective before the first (uneven)
+                # point-to-point batch creates the communicator
+                t = D.zeros(1)
+                dist.all_reduce(t, group=group)
         else:
             self.rank, self.size, self.nccl = 0, 1, False
 
