@@ -242,6 +242,10 @@ def run_ours(args):
     us = _time_op(lambda: lib.cprb_pgs_scm_pass(C.byref(lvl0.desc), D.ptr(bp), D.ptr(xp), 1, 0,
                                                 D.stream()), reps, torch)
     kern["pgs_scm_sweep_l0"] = (us, _bytes_sweep(A0.nrows, A0.nnz))
+    bc = Bd.amg.levels[1].b if len(Bd.amg.levels) > 1 else D.empty(A0.nrows)
+    us = _time_op(lambda: lib.cprb_resid_restrict(C.byref(lvl0.desc), D.ptr(bp), D.ptr(xp),
+                                                  D.ptr(bc), D.stream()), reps, torch)
+    kern["resid_restrict_l0"] = (us, A0.nnz * 12 + A0.nrows * 28)
     Fl = B.relaxation
     n_off_l = Fl.L.nnz - nb
     n_off_u = Fl.U.nnz - nb
