@@ -410,6 +410,100 @@ def run_partitioned(args):
         dist.destroy_process_group()
 
 
+def run_c2(args):
+    """Config 2: one AMG V(1,1) cycle on the 128^3 variable-coefficient
+    pressure system (AMG stage alone, 1 GPU; src/amg.py:228-267)."""
+    import ctypes as C
+
+    import torch
+
+    import paper_2201_01970_b200 as P
+    from paper_2201_01970_b200 import _native as N
+    from paper_2201_01970_b200 import device as D
+
+    torch.cuda.set_device(0)
+    t0 = time.perf_counter()
+    A = P.problems.pressure_operator(128, 128, 128)
+    h = P.build_hierarchy(A, P.AmgParams(theta_amg=0.0, cycle="v"))
+    dev = h.device(1)
+    t_setup = time.perf_counter() - t0
+    n = A.nrows
+    r = D.upload(np.ones(n))
+    z = D.empty(n)
+    cache = C.c_void_p()
+    N.check(N.lib().cprb_graph_cache_create(C.byref(cache)))
+    cyc = lambda: N.check(N.lib().cprb_amg_cycle_graph(cache, C.byref(dev.desc), D.ptr(r), D.ptr(z),
+                                                       D.stream()))
+    for _ in range(max(args.warmup, 3)):
+        cyc()
+    us = _time_op(cyc, max(args.steps, 10), torch)
+    peak, peak_kind = _peaks()
+    lv = h.levels
+    vbytes = sum(2 * _bytes_sweep(l.A.nrows, l.A.nnz) + l.A.nnz * 12 + l.A.nrows * 28
+                 for l in lv[:-1])
+    lvl0 = dev.levels[0]
+    xp = D.zeros(n)
+    us0 = _time_op(lambda: N.lib().cprb_pgs_scm_pass(C.byref(lvl0.desc), D.ptr(r), D.ptr(xp), 1, 0,
+                                                     D.stream()), 20, torch)
+    b0 = _bytes_sweep(n, A.nnz)
+    r_pin = torch.ones(n, dtype=torch.float64).pin_memory()
+    te = []
+    for _ in range(5):
+        t1 = time.perf_counter()
+        _ = P.amg_cycle(h, r_pin).numpy()
+        te.append(time.perf_counter() - t1)
+    ach = vbytes / (us * 1e-6) / 1e9
+    out = {"metric": "AMG V(1,1)-cycle time, 128^3 pressure system (config 2)", "value": round(us / 1e3, 4),
+           "unit": "ms", "n_gpus": 1, "steps": max(args.steps, 10), "warmup": max(args.warmup, 3),
+           "higher_is_better": False, "dtype": "f64", "data": "synthetic (reference generator, seed 0)",
+           "config": {"workload": "128^3 pressure operator, AmgParams(theta_amg=0, cycle='v'), b = ones",
+                      "rows": n, "nnz": int(A.nnz), "levels": len(lv),
+                      "colors": [l.partition.c for l in lv[:-1]]},
+           "e2e": {"value": round(float(np.median(te)) * 1e3, 4), "unit": "ms",
+                   "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n},
+           "roofline": {"bound": "hbm", "kernel": "amg_vcycle (all levels)", "achieved": round(ach, 1),
+                        "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                        "frac": round(ach / peak, 4), "algorithmic_bytes": int(vbytes)},
+           "kernels": {"pgs_scm_sweep_l0": {"us": round(us0, 2), "bytes": int(b0),
+                                            "GB/s": round(b0 / (us0 * 1e-6) / 1e9, 1),
+                                            "frac": round(b0 / (us0 * 1e-6) / 1e9 / peak, 4)}},
+           "setup_s": round(t_setup, 2)}
+    N.lib().cprb_graph_cache_destroy(cache)
+    print(json.dumps(out))
+
+
+def run_c4(args):
+    """Config 4: 10 Newton Jacobians of the SPE10-shaped model through the
+    adaptive-setup sequence solver (src/cpr.py:349-382), mu = 5."""
+    import torch
+
+    import paper_2201_01970_b200 as P
+
+    torch.cuda.set_device(0)
+    nx, ny, nz = args.grid
+    t0 = time.perf_counter()
+    seq = P.generate_blackoil_like_sequence(nx, ny, nz, 10, 0.01, 0)
+    systems = [(A, torch.from_numpy(b).cuda()) for A, b in seq.systems]
+    t_gen = time.perf_counter() - t0
+    cfg = P.SolverConfig(theta=0.0, theta_amg=0.0, cycle=args.cycle)
+    P.ascpr_gmres_sequence(systems[:1], 5, cfg, keep_solutions=False)   # warm-up (module init)
+    res = P.ascpr_gmres_sequence(systems, 5, cfg, keep_solutions=False)
+    recs = res.records
+    out = {"metric": "ASCPR sequence: SOLVE and SETUP time over 10 Newton Jacobians (config 4)",
+           "value": round(res.solve_time * 1e3, 3), "unit": "ms", "n_gpus": 1, "steps": 1,
+           "warmup": 1, "higher_is_better": False, "dtype": "f64",
+           "data": "synthetic (reference generator restated bitwise: seed 0, drift 0.01)",
+           "config": {"workload": f"10 SPE10-shaped {nx}x{ny}x{nz} systems, mu = 5, "
+                                  f"SolverConfig(theta=0, theta_amg=0, cycle='{args.cycle}')"},
+           "setup_calls": res.setup_calls, "setup_s": round(res.setup_time, 3),
+           "solve_ms_per_system": round(res.solve_time * 1e3 / len(recs), 3),
+           "inner": [r.inner for r in recs], "outer": [r.outer for r in recs],
+           "rebuilt": [bool(r.rebuilt) for r in recs],
+           "converged": all(r.converged for r in recs), "generate_s": round(t_gen, 2),
+           "note": "solve time includes uploading each new Jacobian (the reused preconditioner keeps its build matrix)"}
+    print(json.dumps(out))
+
+
 def _ncu_traffic(kernel: str, grid):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`
     (a bench kernel family) from the committed ncu --set full capture
@@ -543,11 +637,17 @@ def main():
     ap.add_argument("--grid", type=_grid, default=(60, 220, 85))
     ap.add_argument("--cycle", default="v", choices=["v", "k"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--config", default="c3", choices=["c3", "c2", "c4"],
+                    help="c2: AMG V-cycle on 128^3 pressure; c4: ASCPR 10-system sequence")
     ap.add_argument("--partition", action="store_true",
                     help="row-slab partition ONE system over the N ranks (strong scaling)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.config == "c2":
+        run_c2(args)
+    elif args.config == "c4":
+        run_c4(args)
     elif args.partition:
         run_partitioned(args)
     else:

@@ -124,7 +124,7 @@ typedef struct cprb_amg_level {
   double* tmp;                 /* dev work, n (snapshot sweeps) */
   const int32_t* color_width;  /* host|NULL, 2*ncolors: max lane_len, max lane_len_lo per colour */
   int32_t restrict_width;      /* max row length of restrict_op (0 = unknown) */
-  int32_t pad_;
+  int32_t one_cta;             /* 1 = V-cycle runs this level's passes in one CTA (x in smem) */
 } cprb_amg_level;
 
 /* Device pointers of one coarse level for the persistent V-cycle tail
@@ -299,6 +299,15 @@ int cprb_axpy(int64_t n, double alpha, const double* x, const double* y, double*
 int cprb_div_host(int64_t n, const double* x, double h, double* out, void* stream);
 /* out = x / (*h_dev)  (src/cpr.py:262 V[0] = r / beta) */
 int cprb_div_scalar(int64_t n, const double* x, const double* h_dev, double* out, void* stream);
+
+/* Device SELL-32 packing of a (block) CSR matrix in natural row order
+ * (uploads of new Jacobians, src/sparse.py:203-308 layout -> cprb_sell):
+ * row_ptr/col_idx int64 and values (nnz*b*b) are device copies of the CSR
+ * arrays; slice_ptr (host-computed widths) is on the device; cols/vals are
+ * zero-filled outputs of slice_ptr[nslices] (x b*b) entries. */
+int cprb_pack_bsr_sell(int64_t nrows, int32_t b, const int64_t* row_ptr, const int64_t* col_idx,
+                       const double* values, const int64_t* slice_ptr, int32_t* cols,
+                       double* vals, void* stream);
 
 /* ---- slab-partitioned solve (paper_2201_01970_b200/partition.py) ----
  * Each rank owns a contiguous range of block rows; operators read a column

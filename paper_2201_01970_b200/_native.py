@@ -36,7 +36,7 @@ class AmgLevel(C.Structure):
                 ("color_rows", i32p), ("color_snapshot", u8p), ("smoother", Sell),
                 ("diag", vp), ("restrict_op", Sell), ("aggp", vp), ("b", vp), ("x", vp),
                 ("tmp", vp), ("color_width", i32p), ("restrict_width", C.c_int32),
-                ("pad_", C.c_int32)]
+                ("one_cta", C.c_int32)]
 
 
 class TailLevel(C.Structure):
@@ -95,6 +95,7 @@ _SIGS = {
     "cprb_bilu_apply": (C.c_int, [C.POINTER(Bilu), vp, vp, vp, vp]),
     "cprb_cpr_apply": (C.c_int, [C.POINTER(Cpr), vp, vp, vp]),
     "cprb_wave_set_log": (C.c_int, [vp]),
+    "cprb_pack_bsr_sell": (C.c_int, [C.c_int64, C.c_int32, vp, vp, vp, vp, vp, vp, vp]),
     "cprb_stage2_residual": (C.c_int, [vp, C.c_int32, vp, vp, vp, vp]),
     "cprb_pgs_scm_color": (C.c_int, [vp, C.c_int32, vp, vp, C.c_int32, vp, C.c_int32, vp, vp, vp]),
     "cprb_seg_partials": (C.c_int, [C.c_int64, C.c_int64, vp, vp, vp, vp, vp, vp]),

@@ -252,6 +252,7 @@ def _permuted_rows_sell(A, perm: np.ndarray, inv: np.ndarray):
     return D.pack_sell(lane_row, lane_ptr, cols, vals, 1, n)
 
 
+LV1_ROWS = 0  # coarse levels at most this large run each V-cycle pass in ONE CTA (csrc/amg.cu k_lv_fwd/k_lv_bwd)
 TAIL_ROWS = 0  # levels at most this large run in the persistent tail kernel (0 = off)
 TAIL3_CTAS = 16          # cluster size of the smem-resident tail
 TAIL3_SMEM_MAX = 200 * 1024  # per-CTA packed bytes (dynamic shared memory)
@@ -295,6 +296,9 @@ class DeviceAmg:
             dl.desc.restrict_op = R.desc
             dl.desc.restrict_width = int(R.host.lane_len.max()) if R.host.lane_len.size else 0
             dl.desc.aggp = D.ptr(aggp)
+            lim = int(os.environ.get("CPRB_LV1_ROWS", str(LV1_ROWS)))
+            dl.desc.one_cta = 1 if (l >= 1 and lvl.A.nrows <= lim and dl.desc.ncolors > 1
+                                    and not dl.snapshot.any()) else 0
             self.levels.append(dl)
             self.restrict.append(R)
             self.aggp.append(aggp)

@@ -653,6 +653,240 @@ int pgs_pass(const cprb_amg_level& L, const double* b_in, double* x, int dir, in
   return check_launch("pgs pass");
 }
 
+// ---------------------------------------------------------------------------
+// Single-CTA level passes (coarse levels of the V-cycle).  A coarse level's
+// colour sweeps cost one dependent launch each (~3 us) while its work is a
+// few microseconds, so a level with at most a few thousand rows runs its
+// whole forward pass (zero-guess colour sweeps + fused residual/restriction)
+// in ONE CTA and its whole backward pass (prolongation + reverse colour
+// sweeps) in another: x lives in shared memory, colours are separated by
+// __syncthreads, and every row is summed exactly as k_sweep /
+// k_resid_restrict sum it (bitwise identical results).
+constexpr int LV_THREADS = 256;
+constexpr int LV_MAXC = 32;
+
+struct LvArgs {
+  cprb_sell S;  // smoother (off-diagonals, colour slices)
+  cprb_sell R;  // restriction (aggregate lane pairs, original column order)
+  const double* diag;
+  const int32_t* aggp;
+  const double* b;
+  double* x;
+  int n, nc, fused;
+  int cs[LV_MAXC + 1];
+  int cr[LV_MAXC + 1];
+  double* bc;         // forward: next level's b (or the coarse b)
+  double* xn;         // forward: next level's x (fused first colour) or nullptr
+  const double* dn;
+  int c0n;
+  const double* xc;   // backward: coarse correction
+};
+
+// reduceat row sum a0 + pairwise8(rest) over a generic x (shared memory)
+__device__ __forceinline__ double rr_row_gen(const cprb_sell& R, int64_t base, int len,
+                                             const double* x) {
+  if (len > 129) {
+    auto f = [&](int m) -> double {
+      const int64_t e = base + (int64_t)m * 32;
+      return __ldg(R.vals + e) * x[__ldg(R.cols + e)];
+    };
+    return segsum_rt(f, len);
+  }
+  if (len <= 0) return 0.0;
+  const int nr = len - 1;
+  const int nf = nr >= 8 ? (nr & ~7) : 0;
+  double a0 = 0.0, s = -0.0, r8[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) r8[k] = 0.0;
+  for (int p = 0; p < len; ++p) {
+    const int64_t e = base + (int64_t)p * 32;
+    const double v = __ldg(R.vals + e) * x[__ldg(R.cols + e)];
+    if (p == 0) {
+      a0 = v;
+      continue;
+    }
+    const int q = p - 1;
+    if (q < nf) {
+      if (q < 8) r8[q & 7] = v;
+      else r8[q & 7] = r8[q & 7] + v;
+      if (q == nf - 1) s = ((r8[0] + r8[1]) + (r8[2] + r8[3])) + ((r8[4] + r8[5]) + (r8[6] + r8[7]));
+    } else {
+      s = s + v;
+    }
+  }
+  return a0 + s;
+}
+
+// one row of a colour: static data prefetched into registers (a colour's
+// rows are loaded while the previous colour is being computed)
+constexpr int LV_CH = 16;
+struct LvRow {
+  int row, len;
+  int64_t base;
+  double d, bi;
+  int c[LV_CH];
+  double v[LV_CH];
+};
+
+template <int ZG>
+__device__ __forceinline__ LvRow lv_load(const LvArgs& a, int k, int r) {
+  LvRow q;
+  q.row = -1;
+  q.len = 0;
+  if (k < 0 || k >= a.nc) return q;
+  const int r0 = a.cr[k];
+  if (r >= a.cr[k + 1] - r0) return q;
+  const int w = a.cs[k] + (r >> 5), lane = r & 31;
+  const int lid = w * 32 + lane;
+  q.len = ZG ? __ldg(a.S.lane_len_lo + lid) : __ldg(a.S.lane_len + lid);
+  q.base = __ldg(a.S.slice_ptr + w) + lane;
+  q.row = r0 + r;
+  q.d = __ldg(a.diag + q.row);
+  q.bi = __ldcg(a.b + q.row);
+#pragma unroll
+  for (int m = 0; m < LV_CH; ++m)
+    if (m < q.len) {
+      q.c[m] = __ldg(a.S.cols + q.base + (int64_t)m * 32);
+      q.v[m] = __ldg(a.S.vals + q.base + (int64_t)m * 32);
+    }
+  return q;
+}
+
+__device__ __forceinline__ void lv_row(const LvArgs& a, const LvRow& q, double* sx) {
+  if (q.row < 0) return;
+  double acc = 0.0;
+#pragma unroll
+  for (int m = 0; m < LV_CH; ++m)
+    if (m < q.len) acc = acc + q.v[m] * sx[q.c[m]];
+  for (int m = LV_CH; m < q.len; ++m) {
+    const int64_t e = q.base + (int64_t)m * 32;
+    acc = acc + __ldg(a.S.vals + e) * sx[__ldg(a.S.cols + e)];
+  }
+  sx[q.row] = (q.bi - acc) / q.d;
+}
+
+// colours kbeg, kbeg+dk, ... (nk of them); the first row of every thread in
+// the next colour is prefetched before this colour's barrier
+template <int ZG>
+__device__ __forceinline__ void lv_pass(const LvArgs& a, int kbeg, int dk, int nk, double* sx) {
+  LvRow cur = lv_load<ZG>(a, kbeg, threadIdx.x);
+  for (int t = 0; t < nk; ++t) {
+    const int k = kbeg + t * dk;
+    const LvRow nxt = lv_load<ZG>(a, t + 1 < nk ? k + dk : -1, threadIdx.x);
+    lv_row(a, cur, sx);
+    const int nr = a.cr[k + 1] - a.cr[k];
+    for (int r = threadIdx.x + LV_THREADS; r < nr; r += LV_THREADS) lv_row(a, lv_load<ZG>(a, k, r), sx);
+    __syncthreads();
+    cur = nxt;
+  }
+}
+
+__global__ void __launch_bounds__(LV_THREADS, 1) k_lv_fwd(const LvArgs a) {
+  extern __shared__ double sx[];
+  pdl_trigger();
+  AmgMark mk;
+  mk.start(6);
+  pdl_wait();
+  mk.waited();
+  int k0 = 0;
+  if (a.fused) {  // colour 0 already computed by the previous restriction
+    for (int i = threadIdx.x; i < a.cr[1]; i += LV_THREADS) sx[i] = __ldcg(a.x + i);
+    k0 = 1;
+  }
+  __syncthreads();
+  lv_pass<1>(a, k0, 1, a.nc - k0, sx);
+  for (int i = threadIdx.x; i < a.n; i += LV_THREADS) a.x[i] = sx[i];
+  // fused residual + restriction (k_resid_restrict), x from shared memory:
+  // a row's entries are loaded in one batch, then summed in reduceat order
+  const int lane = threadIdx.x & 31;
+  for (int w = threadIdx.x >> 5; w < a.R.nslices; w += LV_THREADS / 32) {
+    const int lid = w * 32 + lane;
+    const int row = __ldg(a.R.lane_row + lid);
+    const int len = row >= 0 ? __ldg(a.R.lane_len + lid) : 0;
+    const int64_t base = __ldg(a.R.slice_ptr + w) + lane;
+    const int out = ((lane & 1) == 0) ? __ldg(a.R.agg_out + w * 16 + (lane >> 1)) : -1;
+    constexpr int P = 32;
+    int c[P];
+    double e[P];
+#pragma unroll
+    for (int m = 0; m < P; ++m)
+      if (m < len) {
+        c[m] = __ldg(a.R.cols + base + (int64_t)m * 32);
+        e[m] = __ldg(a.R.vals + base + (int64_t)m * 32);
+      }
+    double res = 0.0;
+    if (row >= 0) {
+      const double bi = __ldcg(a.b + row);
+      double t;
+      if (len <= P) {
+#pragma unroll
+        for (int m = 0; m < P; ++m) e[m] = (m < len) ? e[m] * sx[c[m]] : 0.0;
+        t = segsum_masked<P>(e, len);
+      } else {
+        t = rr_row_gen(a.R, base, len, sx);
+      }
+      res = bi - t;
+    }
+    const double other = __shfl_down_sync(CPRB_FULL, res, 1);
+    if ((lane & 1) == 0 && out >= 0) {
+      const double bcv = (0.0 + res) + other;
+      a.bc[out] = bcv;
+      if (a.xn && out < a.c0n) a.xn[out] = (bcv - 0.0) / a.dn[out];
+    }
+  }
+  mk.end();
+}
+
+__global__ void __launch_bounds__(LV_THREADS, 1) k_lv_bwd(const LvArgs a) {
+  extern __shared__ double sx[];
+  pdl_trigger();
+  AmgMark mk;
+  mk.start(7);
+  pdl_wait();
+  mk.waited();
+  for (int i = threadIdx.x; i < a.n; i += LV_THREADS)
+    sx[i] = __ldcg(a.x + i) + __ldcg(a.xc + __ldg(a.aggp + i));  // prolongation (k_prolong)
+  __syncthreads();
+  lv_pass<0>(a, a.nc - 1, -1, a.nc, sx);
+  for (int i = threadIdx.x; i < a.n; i += LV_THREADS) a.x[i] = sx[i];
+  mk.end();
+}
+
+static LvArgs lv_args(const cprb_amg_level& L) {
+  LvArgs a = {};
+  a.S = L.smoother;
+  a.R = L.restrict_op;
+  a.diag = L.diag;
+  a.aggp = L.aggp;
+  a.b = L.b;
+  a.x = L.x;
+  a.n = L.n;
+  a.nc = L.ncolors;
+  for (int k = 0; k <= L.ncolors && k <= LV_MAXC; ++k) {
+    a.cs[k] = L.color_slices[k];
+    a.cr[k] = L.color_rows[k];
+  }
+  return a;
+}
+
+static bool lv_ok(const cprb_amg_level& L) {
+  if (!L.one_cta || L.ncolors < 2 || L.ncolors > LV_MAXC) return false;
+  if ((size_t)L.n * sizeof(double) > 200 * 1024) return false;
+  if (L.color_snapshot)
+    for (int k = 0; k < L.ncolors; ++k)
+      if (L.color_snapshot[k]) return false;
+  return true;
+}
+
+static void lv_attr() {
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(k_lv_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_lv_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    done = true;
+  }
+}
+
 int amg_vcycle(const cprb_amg& h, const double* r, double* z, cudaStream_t st) {
   const int nl = h.nlevels;
   if (nl <= 1) {
@@ -667,6 +901,20 @@ int amg_vcycle(const cprb_amg& h, const double* r, double* z, cudaStream_t st) {
   int fused = 0;  // colour 0 of this level was computed by the previous restriction
   for (int l = 0; l < ts; ++l) {
     const cprb_amg_level& L = h.levels[l];
+    if (l >= 1 && lv_ok(L)) {
+      lv_attr();
+      LvArgs a = lv_args(L);
+      a.fused = fused;
+      a.bc = (l + 1 < nl - 1) ? h.levels[l + 1].b : h.coarse_b;
+      const cprb_amg_level* next =
+          (l + 1 < ts && h.levels[l + 1].ncolors > 1) ? &h.levels[l + 1] : nullptr;
+      a.xn = next ? next->x : nullptr;
+      a.dn = next ? next->diag : nullptr;
+      a.c0n = next ? next->color_rows[1] : 0;
+      launch_pdl(k_lv_fwd, 1, LV_THREADS, (size_t)L.n * sizeof(double), st, a);
+      fused = next ? 1 : 0;
+      continue;
+    }
     int rc = pgs_pass(L, L.b, L.x, 0, 1, l == 0 ? r : nullptr, h.in_stride, h.perm0, nullptr, st,
                       fused);
     if (rc) return rc;
@@ -685,6 +933,12 @@ int amg_vcycle(const cprb_amg& h, const double* r, double* z, cudaStream_t st) {
   for (int l = ts - 1; l >= 0; --l) {
     const cprb_amg_level& L = h.levels[l];
     const double* xc = (l + 1 < nl - 1) ? h.levels[l + 1].x : h.coarse_x;
+    if (l >= 1 && lv_ok(L)) {
+      LvArgs a = lv_args(L);
+      a.xc = xc;
+      launch_pdl(k_lv_bwd, 1, LV_THREADS, (size_t)L.n * sizeof(double), st, a);
+      continue;
+    }
     launch_pdl(k_prolong, nblk(L.n, 256), 256, 0, st, L.n, L.aggp, xc, L.x);
     int rc = pgs_pass(L, L.b, L.x, 1, 0, nullptr, 0, h.perm0, l == 0 ? z : nullptr, st);
     if (rc) return rc;

@@ -152,3 +152,36 @@ extern "C" int cprb_stage2_residual(const cprb_sell* A, int32_t b, const double*
                                     const double* r, double* r2, void* stream) {
   return bsr_op(2, *A, b, zp, r, r2, nullptr, nullptr, (cudaStream_t)stream);
 }
+
+// device SELL-32 packing of a BSR matrix in natural row order (the layout of
+// device.sell_rows / pack_sell): entry m of row i lands at slot
+// slice_ptr[i/32] + 32 m + i%32; values verbatim, padding left as zeros
+__global__ void k_pack_bsr_sell(int64_t nrows, int bb, const int64_t* __restrict__ rp,
+                                const int64_t* __restrict__ ci, const double* __restrict__ v,
+                                const int64_t* __restrict__ slice_ptr, int32_t* __restrict__ cols,
+                                double* __restrict__ vals) {
+  const int64_t row = blockIdx.x * (int64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= nrows) return;
+  const int64_t e0 = rp[row], e1 = rp[row + 1];
+  const int64_t sb = slice_ptr[row >> 5];
+  const int l = (int)(row & 31);
+  for (int64_t e = e0; e < e1; ++e) {
+    const int64_t slot = sb + (e - e0) * 32 + l;
+    if (lane == 0) cols[slot] = (int32_t)ci[e];
+    for (int q = lane; q < bb; q += 32)
+      vals[(slot - l) * bb + (int64_t)q * 32 + l] = v[e * bb + q];
+  }
+}
+
+extern "C" int cprb_pack_bsr_sell(int64_t nrows, int32_t b, const int64_t* row_ptr,
+                                  const int64_t* col_idx, const double* values,
+                                  const int64_t* slice_ptr, int32_t* cols, double* vals,
+                                  void* stream) {
+  if (nrows <= 0) return CPRB_OK;
+  const int per = 8;  // rows (warps) per CTA
+  const int64_t grid = (nrows + per - 1) / per;
+  k_pack_bsr_sell<<<(unsigned)grid, per * 32, 0, (cudaStream_t)stream>>>(
+      nrows, b * b, row_ptr, col_idx, values, slice_ptr, cols, vals);
+  return check_launch("pack bsr sell");
+}

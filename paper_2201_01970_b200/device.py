@@ -213,6 +213,49 @@ def sell_rows(ptr_, cols, vals, bs, nrows) -> SellHost:
     return pack_sell(lane_row, lp, cols, vals, bs, nrows)
 
 
+class _PackedSell:
+    """SELL-32 of a (block) CSR in natural row order, packed ON the device
+    from the raw CSR arrays (csrc/spmv.cu k_pack_bsr_sell): the upload of a
+    new Jacobian is one H2D copy of the CSR plus one kernel, not a host
+    repack.  Same layout and values as sell_rows()."""
+
+    def __init__(self, A, bs: int):
+        t = torch()
+        n = int(A.nrows)
+        rp = np.ascontiguousarray(A.row_ptr, dtype=np.int64)
+        lens = np.diff(rp)
+        L = -(-n // 32) * 32
+        lp = np.zeros(L, dtype=np.int64)
+        lp[:n] = lens
+        ns = L // 32
+        width = lp.reshape(ns, 32).max(axis=1) if ns else np.zeros(0, dtype=np.int64)
+        slice_ptr = np.zeros(ns + 1, dtype=np.int64)
+        np.cumsum(width * 32, out=slice_ptr[1:])
+        total = int(slice_ptr[-1])
+        bb = bs * bs
+        lane_row = np.full(L, -1, dtype=np.int32)
+        lane_row[:n] = np.arange(n, dtype=np.int32)
+        self.t = {"slice_ptr": upload(slice_ptr), "lane_row": upload(lane_row),
+                  "lane_len": upload(lp.astype(np.int32)),
+                  "cols": t.zeros(max(total, 1), dtype=t.int32, device="cuda"),
+                  "vals": t.zeros(max(total * bb, 1), dtype=t.float64, device="cuda")}
+        nnz = int(rp[-1])
+        if n and nnz:
+            rp_d = upload(rp)
+            ci_d = upload(np.ascontiguousarray(A.col_idx, dtype=np.int64))
+            v_d = upload(np.ascontiguousarray(A.values, dtype=np.float64).reshape(-1))
+            N.check(N.lib().cprb_pack_bsr_sell(n, bs, ptr(rp_d), ptr(ci_d), ptr(v_d),
+                                               ptr(self.t["slice_ptr"]), ptr(self.t["cols"]),
+                                               ptr(self.t["vals"]), stream()))
+            del rp_d, ci_d, v_d
+        self.host = None
+        self.desc = N.Sell(ns, n, ptr(self.t["slice_ptr"]), ptr(self.t["lane_row"]),
+                           ptr(self.t["lane_len"]), 0, ptr(self.t["cols"]), ptr(self.t["vals"]), 0)
+
+    def nbytes(self) -> int:
+        return sum(int(v.numel() * v.element_size()) for v in self.t.values())
+
+
 class DeviceMatrix:
     """A CsrMatrix / BlockCsrMatrix resident on the device (SELL-32)."""
 
@@ -221,11 +264,7 @@ class DeviceMatrix:
         bs = int(getattr(A, "block_size", 1))
         self.b = bs
         self.nrows = int(A.nrows)
-        vals = np.asarray(A.values, dtype=np.float64)
-        if bs == 1:
-            vals = vals.reshape(-1)
-        self.sell = SellDev(sell_rows(np.asarray(A.row_ptr, dtype=np.int64),
-                                      np.asarray(A.col_idx), vals, bs, A.nrows))
+        self.sell = _PackedSell(A, bs)
 
     def desc_ref(self):
         return C.byref(self.sell.desc)

@@ -76,6 +76,20 @@ def test_spmv_c1_rhs_and_long_rows(gpu):
     del gen
 
 
+def test_device_sell_packing_matches_host_layout(gpu, rng):
+    """Jacobian uploads pack SELL-32 on the device (csrc/spmv.cu
+    k_pack_bsr_sell): identical arrays to the host packer."""
+    from paper_2201_01970_b200 import device as D
+    for M in (_bsr(random_block(rng, 333, 3)), _csr(random_sparse(rng, 517))):
+        bs = int(getattr(M, "block_size", 1))
+        vals = np.asarray(M.values, dtype=np.float64)
+        h = D.sell_rows(np.asarray(M.row_ptr, dtype=np.int64), np.asarray(M.col_idx),
+                        vals if bs > 1 else vals.reshape(-1), bs, M.nrows)
+        d = D._PackedSell(M, bs)
+        for k in ("slice_ptr", "lane_row", "lane_len", "cols", "vals"):
+            assert np.array_equal(d.t[k].cpu().numpy(), np.asarray(getattr(h, k))), k
+
+
 def test_spmv_api_edges(gpu):
     A = P.CsrMatrix(3, 3, [0, 0, 0, 0], [], [])
     assert np.array_equal(P.spmv(A, np.ones(3)), np.zeros(3))
@@ -217,6 +231,29 @@ def test_vcycle_persistent_tail_bitwise(gpu, monkeypatch, tail_rows):
         dev1 = h1.device()
         assert dev1.desc.tail_mode == 3 and dev1.desc.tail_start < len(h1.levels) - 1
         monkeypatch.delenv("CPRB_TAIL_ROWS")
+        assert np.array_equal(z0, z1)
+
+
+@pytest.mark.parametrize("lv_rows", ["9000", "25000"])
+def test_vcycle_one_cta_levels_bitwise(gpu, monkeypatch, lv_rows):
+    """Coarse levels run as one-CTA passes (csrc/amg.cu k_lv_fwd / k_lv_bwd,
+    x in shared memory) with the per-colour kernels' arithmetic: bitwise
+    equal cycles."""
+    A, _ = _c1()
+    (A2, _), = P.generate_blackoil_like_sequence(40, 30, 20, 1, 0.01, 2).systems
+    rng = np.random.default_rng(12)
+    for M in (A, A2):
+        cfg = P.SolverConfig(theta=0.0, theta_amg=0.0, cycle="v")
+        monkeypatch.setenv("CPRB_LV1_ROWS", "0")
+        h0 = P.build_hierarchy(P.pressure_matrix(M), cfg.amg_params())
+        r = rng.standard_normal(M.nrows)
+        z0 = P.amg_cycle(h0, r)
+        assert not any(dl.desc.one_cta for dl in h0.device().levels)
+        monkeypatch.setenv("CPRB_LV1_ROWS", lv_rows)
+        h1 = P.build_hierarchy(P.pressure_matrix(M), cfg.amg_params())
+        z1 = P.amg_cycle(h1, r)
+        assert sum(dl.desc.one_cta for dl in h1.device().levels) >= 2
+        monkeypatch.delenv("CPRB_LV1_ROWS")
         assert np.array_equal(z0, z1)
 
 
