@@ -263,7 +263,7 @@ __device__ __noinline__ double rr_row_far(const cprb_sell& R, int64_t base, int 
 }
 
 template <int PRE>
-__global__ void __launch_bounds__(256, PRE <= 16 ? 4 : 2)
+__global__ void __launch_bounds__(256, PRE <= 8 ? 6 : (PRE <= 16 ? 4 : 2))
     k_resid_restrict(const cprb_sell R, const double* __restrict__ b,
                      const double* __restrict__ x, double* __restrict__ bc,
                      double* __restrict__ xn, const double* __restrict__ dn, int c0_rows) {
@@ -299,12 +299,12 @@ __global__ void __launch_bounds__(256, PRE <= 16 ? 4 : 2)
     if (len <= PRE) {
       double e[PRE];
 #pragma unroll
-      for (int m = 0; m < PRE; ++m) e[m] = (m < len) ? v[m] * __ldcg(x + c[m]) : 0.0;
+      for (int m = 0; m < PRE; ++m) e[m] = (m < len) ? v[m] * __ldg(x + c[m]) : 0.0;
       t = segsum_masked<PRE>(e, len);
     } else {
       t = rr_row_far(R, base, len, x);
     }
-    res = __ldcg(b + row) - t;
+    res = __ldg(b + row) - t;
   }
   const double other = __shfl_down_sync(CPRB_FULL, res, 1);
   if ((lane & 1) == 0 && out >= 0) {
