@@ -63,7 +63,7 @@ __device__ __forceinline__ double bsr_row_long(const cprb_sell& A, int64_t base,
 }
 
 template <int B, int MODE>
-__global__ void __launch_bounds__(BSR_WARPS * 32, 4)
+__global__ void __launch_bounds__(BSR_WARPS * 32, 5)
     k_bsr(const cprb_sell A, const double* __restrict__ x, const double* __restrict__ rhs,
           double* __restrict__ out, int32_t* flag, double* __restrict__ sent,
           double* __restrict__ sent2, const int32_t* __restrict__ out_idx,
