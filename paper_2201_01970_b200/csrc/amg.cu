@@ -86,8 +86,11 @@ __device__ __forceinline__ double gs_acc_from(const cprb_sell& S, int64_t base, 
   return acc;
 }
 
+#ifndef SWEEP_MINB
+#define SWEEP_MINB 1
+#endif
 template <int ZG, int GATHER, int SCATTER, int SWEEP_PRE>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, SWEEP_MINB)
     k_sweep(const cprb_sell S, int s0, int s1, int r0, int r1, const double* __restrict__ diag,
             double* b, const double* __restrict__ gsrc, int gstride,
             const int32_t* __restrict__ perm, const double* xin, double* xout,
