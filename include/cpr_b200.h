@@ -155,7 +155,7 @@ typedef struct cprb_amg {
   int32_t in_stride;                /* residual stride of the level-0 input (b of BSR, 1 scalar) */
   int32_t cycle;                    /* 0 = V, 1 = K */
   int32_t use_fcg;                  /* K-cycle Krylov flavour */
-  double* kwork;                    /* dev work for the K-cycle (see engine) */
+  void* kwork;                       /* K-cycle plan (cprb_kcycle_create) or NULL; used when cycle = 1 */
   int64_t kwork_len;
   /* persistent tail: levels >= tail_start (and the coarse solve) run in one
    * cluster-wide kernel; tail_start >= nlevels-1 disables it. */
@@ -252,6 +252,15 @@ int cprb_coarse_solve(const cprb_amg* h, const double* b, double* x, void* strea
 int cprb_resid_restrict(const cprb_amg_level* lvl, const double* b, const double* x, double* bc,
                         void* stream);
 int cprb_prolong(const cprb_amg_level* lvl, const double* xc, double* x, void* stream);
+
+/* src/amg.py:177-196, :245-267  device K-cycle plan (FCG flavour): workspace
+ * for every level and the level matrices in permuted row order with the
+ * reference's column order (level_spmv: host array of nlevels-1 descriptors;
+ * entry 0 unused).  With h->kwork = plan and h->cycle = 1, cprb_amg_cycle /
+ * cprb_cpr_apply run the K-cycle without host synchronisation. */
+int cprb_kcycle_create(const cprb_amg* h, const cprb_sell* level_spmv, int32_t pre_sweeps,
+                       int32_t post_sweeps, void** plan);
+int cprb_kcycle_destroy(void* plan);
 
 /* src/ilu.py:196-223  z = U^{-1} L^{-1} r (level-ordered, sync-free). */
 int cprb_bilu_apply(const cprb_bilu* F, const double* r, double* z, double* work_l,

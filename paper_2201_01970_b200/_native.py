@@ -96,6 +96,8 @@ _SIGS = {
     "cprb_cpr_apply": (C.c_int, [C.POINTER(Cpr), vp, vp, vp]),
     "cprb_wave_set_log": (C.c_int, [vp]),
     "cprb_pack_bsr_sell": (C.c_int, [C.c_int64, C.c_int32, vp, vp, vp, vp, vp, vp, vp]),
+    "cprb_kcycle_create": (C.c_int, [vp, vp, C.c_int32, C.c_int32, vp]),
+    "cprb_kcycle_destroy": (C.c_int, [vp]),
     "cprb_stage2_residual": (C.c_int, [vp, C.c_int32, vp, vp, vp, vp]),
     "cprb_pgs_scm_color": (C.c_int, [vp, C.c_int32, vp, vp, C.c_int32, vp, C.c_int32, vp, vp, vp]),
     "cprb_seg_partials": (C.c_int, [C.c_int64, C.c_int64, vp, vp, vp, vp, vp, vp]),

@@ -600,9 +600,41 @@ class DeviceAmg:
         x = self._cycle_at(0, b0, bool(self.desc.use_fcg), cycle)
         z[self._perm0_t] = x
 
+    # -- K-cycle on the device (csrc/kcycle.cu): no host synchronisation ---------
+    def kdesc(self):
+        """Descriptor of the device K-cycle (FCG flavour), or None when the
+        host-driven path is required (FGMRES flavour, CPRB_HOST_KCYCLE=1)."""
+        if getattr(self, "_kdesc", None) is not None:
+            return self._kdesc
+        if not self.desc.use_fcg or os.environ.get("CPRB_HOST_KCYCLE", "0") == "1":
+            return None
+        L = self.nlevels
+        arr = (N.Sell * max(L - 1, 1))()
+        for l in range(1, L - 1):
+            arr[l] = self._kspmv(l).desc
+        h = C.c_void_p()
+        p = self.h.params
+        N.check(N.lib().cprb_kcycle_create(C.byref(self.desc), arr, p.pre_sweeps, p.post_sweeps,
+                                           C.byref(h)))
+        self._kplan, self._kspmv_arr = h, arr
+        kd = N.Amg.from_buffer_copy(self.desc)
+        kd.cycle = 1
+        kd.kwork = h.value
+        self._kdesc = kd
+        return kd
+
+    def __del__(self):
+        try:
+            if getattr(self, "_kplan", None):
+                N.lib().cprb_kcycle_destroy(self._kplan)
+        except Exception:
+            pass
+
     def cycle(self, r, z, cycle):
         if cycle == "v" and self.native_ok:
             self.vcycle(r, z)
+        elif cycle == "k" and self.kdesc() is not None:
+            N.check(N.lib().cprb_amg_cycle(C.byref(self._kdesc), D.ptr(r), D.ptr(z), D.stream()))
         else:
             self.hostcycle(r, z, cycle)
 

@@ -1016,6 +1016,6 @@ extern "C" int cprb_prolong(const cprb_amg_level* L, const double* xc, double* x
 }
 
 extern "C" int cprb_amg_cycle(const cprb_amg* h, const double* r, double* z, void* stream) {
-  if (h->cycle != 0) return set_error(CPRB_EUNSUPPORTED, "K-cycle is driven from the host layer");
+  if (h->cycle != 0) return kcycle_apply(*h, r, z, (cudaStream_t)stream);
   return amg_vcycle(*h, r, z, (cudaStream_t)stream);
 }

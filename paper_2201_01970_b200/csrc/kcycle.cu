@@ -1,0 +1,273 @@
+// K-cycle (nonlinear AMLI, src/amg.py:245-267) driven from C++ with every
+// Krylov scalar on the device: the coarse recursion of each level is wrapped
+// in two flexible-CG steps (src/amg.py:177-196) whose early exits
+// ("norm2(r) == 0", "pap <= 0 or non-finite") become a device flag that
+// predicates the updates, so an application needs no host synchronisation
+// and can be captured whole into a CUDA graph.  The arithmetic is the host
+// K-cycle's (amg.py DeviceAmg._fcg): the same deterministic dot products
+// (cprb_dot), IEEE scalar divisions and separately rounded axpys, so the
+// device and host K-cycles agree bitwise.
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "device.cuh"
+#include "engine.h"
+
+namespace cprb {
+
+// scalar slots of one FCG frame
+enum { S_ACTIVE = 0, S_RR = 1, S_ZAP = 2, S_PAP1 = 3, S_PAP2 = 4, S_PR = 5, S_ALPHA = 6, S_NS = 8 };
+
+__global__ void k_fcg_init(double* s) { s[S_ACTIVE] = 1.0; }
+
+// if norm2(r) == 0: break
+__global__ void k_fcg_check_rr(double* s) {
+  if (!(sqrt(s[S_RR]) != 0.0)) s[S_ACTIVE] = 0.0;
+}
+
+// pap = s[ip]; if pap <= 0 or non-finite: break; alpha = (p, r) / pap
+__global__ void k_fcg_alpha(double* s, int ip) {
+  const double pap = s[ip];
+  if (s[S_ACTIVE] == 0.0) return;
+  if (pap <= 0.0 || !isfinite(pap)) {
+    s[S_ACTIVE] = 0.0;
+    return;
+  }
+  s[S_ALPHA] = s[S_PR] / pap;
+}
+
+// out = (sign * alpha) * x + y  while the frame is active
+__global__ void k_axpy_alpha(int n, const double* __restrict__ s, double sign,
+                             const double* __restrict__ x, const double* y, double* out) {
+  if (s[S_ACTIVE] == 0.0) return;
+  const double a = sign * s[S_ALPHA];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = a * x[i] + y[i];
+}
+
+// p = p - (dot(z, ap_j) / pap_j) p_j  ==  (-coef) * p_j + z
+__global__ void k_axpy_coef(int n, const double* __restrict__ s, const double* __restrict__ pj,
+                            const double* __restrict__ z, double* __restrict__ out) {
+  if (s[S_ACTIVE] == 0.0) return;
+  const double a = -(s[S_ZAP] / s[S_PAP1]);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = a * pj[i] + z[i];
+}
+
+__global__ void k_kgather(int n, const int32_t* __restrict__ idx, const double* __restrict__ src,
+                          int stride, double* __restrict__ dst) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[(int64_t)stride * idx[i]];
+}
+
+__global__ void k_kscatter(int n, const int32_t* __restrict__ idx, const double* __restrict__ src,
+                           double* __restrict__ dst) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[idx[i]] = src[i];
+}
+
+__global__ void k_kprolong(int n, const int32_t* __restrict__ aggp, const double* __restrict__ xc,
+                           double* __restrict__ x) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = x[i] + xc[aggp[i]];
+}
+
+__global__ void k_kdense(int n, const double* __restrict__ inv, const double* __restrict__ b,
+                         double* __restrict__ x) {
+  const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (w >= n) return;
+  const double* row = inv + (int64_t)w * n;
+  double s = 0.0;
+  for (int c = lane; c < n; c += 32) s = s + row[c] * b[c];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s = s + __shfl_xor_sync(CPRB_FULL, s, o);
+  if (lane == 0) x[w] = s;
+}
+
+// grid for the grid-stride kernels (axpys)
+static inline int kb(int64_t n) {
+  int64_t g = (n + 255) / 256;
+  if (g > 148 * 8) g = 148 * 8;
+  return (int)(g < 1 ? 1 : g);
+}
+// grid covering n threads (one element per thread: gather, scatter,
+// prolongation, dense rows)
+static inline int kfull(int64_t n) {
+  int64_t g = (n + 255) / 256;
+  return (int)(g < 1 ? 1 : g);
+}
+
+struct KPlan {
+  int nl = 0;
+  std::vector<cprb_sell> spmv;  // level matrices (permuted rows, original column order)
+  std::vector<int> n;
+  std::vector<double*> x, r, z1, ap1, z2, p2, ap2, s, rc, b0, x0;
+  double* coarse_x = nullptr;
+  double* partials = nullptr;
+  int32_t* ticket = nullptr;
+  std::vector<void*> allocs;
+  int pre = 1, post = 1;
+
+  double* alloc(size_t n_) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, sizeof(double) * (n_ > 0 ? n_ : 1)) != cudaSuccess) return nullptr;
+    cudaMemset(p, 0, sizeof(double) * (n_ > 0 ? n_ : 1));
+    allocs.push_back(p);
+    return (double*)p;
+  }
+  ~KPlan() {
+    for (void* p : allocs) cudaFree(p);
+  }
+};
+
+static int kdot(const KPlan& P, int n, const double* x, const double* y, double* out,
+                cudaStream_t st) {
+  return cprb_dot(n, x, y, out, P.partials, P.ticket, st);
+}
+
+static int kcycle_at(const KPlan& P, const cprb_amg& h, int l, const double* b, double* x,
+                     cudaStream_t st);
+
+// two flexible-CG steps at level l with the cycle at l as preconditioner;
+// the result is P.x[l]
+static int fcg_at(const KPlan& P, const cprb_amg& h, int l, const double* rhs, cudaStream_t st) {
+  const int n = P.n[l];
+  double* s = P.s[l];
+  double *x = P.x[l], *r = P.r[l], *z1 = P.z1[l], *ap1 = P.ap1[l], *z2 = P.z2[l];
+  double *p2 = P.p2[l], *ap2 = P.ap2[l];
+  k_fcg_init<<<1, 1, 0, st>>>(s);
+  cudaMemsetAsync(x, 0, sizeof(double) * n, st);
+  cudaMemcpyAsync(r, rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, st);
+  int rc;
+  // step 1 (no stored directions: p = z)
+  if ((rc = kdot(P, n, r, r, s + S_RR, st))) return rc;
+  k_fcg_check_rr<<<1, 1, 0, st>>>(s);
+  if ((rc = kcycle_at(P, h, l, r, z1, st))) return rc;
+  if ((rc = bsr_op(0, P.spmv[l], 1, z1, nullptr, ap1, nullptr, nullptr, st))) return rc;
+  if ((rc = kdot(P, n, z1, ap1, s + S_PAP1, st))) return rc;
+  if ((rc = kdot(P, n, z1, r, s + S_PR, st))) return rc;
+  k_fcg_alpha<<<1, 1, 0, st>>>(s, S_PAP1);
+  k_axpy_alpha<<<kb(n), 256, 0, st>>>(n, s, 1.0, z1, x, x);
+  k_axpy_alpha<<<kb(n), 256, 0, st>>>(n, s, -1.0, ap1, r, r);
+  // step 2 (one stored direction)
+  if ((rc = kdot(P, n, r, r, s + S_RR, st))) return rc;
+  k_fcg_check_rr<<<1, 1, 0, st>>>(s);
+  if ((rc = kcycle_at(P, h, l, r, z2, st))) return rc;
+  if ((rc = kdot(P, n, z2, ap1, s + S_ZAP, st))) return rc;
+  k_axpy_coef<<<kb(n), 256, 0, st>>>(n, s, z1, z2, p2);
+  if ((rc = bsr_op(0, P.spmv[l], 1, p2, nullptr, ap2, nullptr, nullptr, st))) return rc;
+  if ((rc = kdot(P, n, p2, ap2, s + S_PAP2, st))) return rc;
+  if ((rc = kdot(P, n, p2, r, s + S_PR, st))) return rc;
+  k_fcg_alpha<<<1, 1, 0, st>>>(s, S_PAP2);
+  k_axpy_alpha<<<kb(n), 256, 0, st>>>(n, s, 1.0, p2, x, x);
+  return check_launch("fcg");
+}
+
+// src/amg.py:245-267 (K): x = cycle_l(b) from a zero guess
+static int kcycle_at(const KPlan& P, const cprb_amg& h, int l, const double* b, double* x,
+                     cudaStream_t st) {
+  const int L = h.nlevels;
+  if (l == L - 1) {
+    k_kdense<<<kfull((int64_t)h.n_coarse * 32), 256, 0, st>>>(h.n_coarse, h.coarse_inv, b, x);
+    return check_launch("k coarse");
+  }
+  const cprb_amg_level& Lv = h.levels[l];
+  int rc;
+  for (int sw = 0; sw < P.pre; ++sw)
+    if ((rc = pgs_pass(Lv, b, x, 0, sw == 0 ? 1 : 0, nullptr, 0, nullptr, nullptr, st))) return rc;
+  double* bc = P.rc[l];
+  if ((rc = cprb_resid_restrict(&Lv, b, x, bc, st))) return rc;
+  const double* ec;
+  if (l + 1 == L - 1) {
+    k_kdense<<<kfull((int64_t)h.n_coarse * 32), 256, 0, st>>>(h.n_coarse, h.coarse_inv, bc,
+                                                           P.coarse_x);
+    ec = P.coarse_x;
+  } else {
+    if ((rc = fcg_at(P, h, l + 1, bc, st))) return rc;
+    ec = P.x[l + 1];
+  }
+  k_kprolong<<<kfull(Lv.n), 256, 0, st>>>(Lv.n, Lv.aggp, ec, x);
+  for (int sw = 0; sw < P.post; ++sw)
+    if ((rc = pgs_pass(Lv, b, x, 1, 0, nullptr, 0, nullptr, nullptr, st))) return rc;
+  return check_launch("k cycle");
+}
+
+int kcycle_apply(const cprb_amg& h, const double* r, double* z, cudaStream_t st) {
+  const KPlan* P = static_cast<const KPlan*>((void*)h.kwork);
+  if (!P) return set_error(CPRB_EINVAL, "K-cycle plan missing (cprb_kcycle_create)");
+  if (h.nlevels <= 1) {
+    k_kgather<<<kfull(h.n_coarse), 256, 0, st>>>(h.n_coarse, h.perm0, r, h.in_stride, P->b0[0]);
+    k_kdense<<<kfull((int64_t)h.n_coarse * 32), 256, 0, st>>>(h.n_coarse, h.coarse_inv, P->b0[0], z);
+    return check_launch("k coarse only");
+  }
+  const int n0 = P->n[0];
+  k_kgather<<<kfull(n0), 256, 0, st>>>(n0, h.perm0, r, h.in_stride, P->b0[0]);
+  int rc = kcycle_at(*P, h, 0, P->b0[0], P->x0[0], st);
+  if (rc) return rc;
+  k_kscatter<<<kfull(n0), 256, 0, st>>>(n0, h.perm0, P->x0[0], z);
+  return check_launch("k cycle apply");
+}
+
+}  // namespace cprb
+
+using namespace cprb;
+
+extern "C" {
+
+int cprb_kcycle_create(const cprb_amg* h, const cprb_sell* level_spmv, int32_t pre_sweeps,
+                       int32_t post_sweeps, void** out) {
+  if (!h || !out) return set_error(CPRB_EINVAL, "null argument");
+  if (!h->use_fcg) return set_error(CPRB_EUNSUPPORTED, "device K-cycle implements the FCG flavour");
+  auto* P = new KPlan();
+  const int L = h->nlevels;
+  P->nl = L;
+  P->pre = pre_sweeps;
+  P->post = post_sweeps;
+  P->n.resize(L);
+  for (int l = 0; l < L - 1; ++l) P->n[l] = h->levels[l].n;
+  P->n[L - 1] = h->n_coarse;
+  P->spmv.assign(level_spmv, level_spmv + (L > 1 ? L - 1 : 0));
+  auto vec = [&](std::vector<double*>& v) { v.assign(L, nullptr); };
+  vec(P->x); vec(P->r); vec(P->z1); vec(P->ap1); vec(P->z2); vec(P->p2); vec(P->ap2);
+  vec(P->s); vec(P->rc); vec(P->b0); vec(P->x0);
+  for (int l = 0; l < L; ++l) {
+    const size_t n = (size_t)P->n[l];
+    if (l >= 1 && l < L - 1) {
+      P->x[l] = P->alloc(n); P->r[l] = P->alloc(n); P->z1[l] = P->alloc(n);
+      P->ap1[l] = P->alloc(n); P->z2[l] = P->alloc(n); P->p2[l] = P->alloc(n);
+      P->ap2[l] = P->alloc(n); P->s[l] = P->alloc(S_NS);
+    }
+    if (l < L - 1) P->rc[l] = P->alloc((size_t)P->n[l + 1]);
+  }
+  P->b0[0] = P->alloc((size_t)P->n[0]);
+  P->x0[0] = P->alloc((size_t)P->n[0]);
+  P->coarse_x = P->alloc((size_t)h->n_coarse);
+  P->partials = P->alloc(CPRB_RED_BLOCKS);
+  {
+    void* t = nullptr;
+    if (cudaMalloc(&t, 64) != cudaSuccess) {
+      delete P;
+      return set_error(CPRB_EDEVICE, "K-cycle ticket allocation");
+    }
+    cudaMemset(t, 0, 64);
+    P->allocs.push_back(t);
+    P->ticket = (int32_t*)t;
+  }
+  for (void* p : P->allocs)
+    if (!p) {
+      delete P;
+      return set_error(CPRB_EDEVICE, "K-cycle workspace allocation");
+    }
+  cudaDeviceSynchronize();
+  *out = P;
+  return check_launch("kcycle create");
+}
+
+int cprb_kcycle_destroy(void* plan) {
+  delete static_cast<KPlan*>(plan);
+  return CPRB_OK;
+}
+
+}  // extern "C"

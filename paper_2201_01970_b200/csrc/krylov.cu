@@ -245,8 +245,8 @@ int cprb_cpr_finish(const cprb_cpr* P, const double* r, double* z, void* stream)
 
 // src/cpr.py:178-186:  zp = AMG(Pi^T r);  r2 = r - A Pi zp;  z = Pi zp + BILU(r2)
 int cprb_cpr_apply(const cprb_cpr* P, const double* r, double* z, void* stream) {
-  if (P->amg.cycle != 0) return set_error(CPRB_EUNSUPPORTED, "K-cycle CPR is driven from the host layer");
-  int rc = amg_vcycle(P->amg, r, P->zp, (cudaStream_t)stream);
+  int rc = P->amg.cycle != 0 ? kcycle_apply(P->amg, r, P->zp, (cudaStream_t)stream)
+                             : amg_vcycle(P->amg, r, P->zp, (cudaStream_t)stream);
   if (rc) return rc;
   return cprb_cpr_finish(P, r, z, stream);
 }

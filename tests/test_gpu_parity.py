@@ -257,6 +257,26 @@ def test_vcycle_one_cta_levels_bitwise(gpu, monkeypatch, lv_rows):
         assert np.array_equal(z0, z1)
 
 
+def test_device_kcycle_bitwise_equals_host_kcycle(gpu):
+    """The C++-driven K-cycle with device Krylov scalars (csrc/kcycle.cu)
+    performs the host-driven K-cycle's arithmetic: bitwise equal."""
+    from paper_2201_01970_b200 import device as D
+    A, _ = _c1()
+    (A2, _), = P.generate_blackoil_like_sequence(24, 20, 12, 1, 0.01, 4).systems
+    rng = np.random.default_rng(21)
+    for M in (A, A2):
+        cfg = P.SolverConfig(theta=0.0, theta_amg=0.0, cycle="k")
+        h = P.build_hierarchy(P.pressure_matrix(M), cfg.amg_params())
+        dev = h.device(1)
+        assert dev.kdesc() is not None and len(h.levels) >= 4
+        r = D.upload(rng.standard_normal(M.nrows))
+        z_host = D.empty(M.nrows)
+        z_dev = D.empty(M.nrows)
+        dev.hostcycle(r, z_host, "k")
+        dev.cycle(r, z_dev, "k")
+        assert np.array_equal(z_host.cpu().numpy(), z_dev.cpu().numpy())
+
+
 def test_cpr_product_form_identity(gpu):
     """Eq. 8 (tests/test_cpr.py:98-118): I - B A = (I - R A)(I - Pi B_P Pi^T A)."""
     rng = np.random.default_rng(20240817)

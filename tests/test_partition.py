@@ -196,3 +196,26 @@ def test_slab_ranks_bitwise_equal_to_one_rank(gpu, world):
         assert hist == one[4]                              # bitwise: GPU-count invariant
         assert np.array_equal(x, one[5])
     assert one[2]
+
+
+@pytest.mark.gpu
+def test_slab_edges_match_single_gpu(gpu):
+    """Unpreconditioned solve, a nonzero initial guess and a zero right-hand
+    side through the partitioned path (N = 1) against gmres_solve."""
+    from paper_2201_01970_b200.partition import gmres_solve_slab
+    A, b = _grid(8, 6, 5)
+    part = SlabPartition(A.nrows, 1, 32)
+    params = P.GmresParams(m=20, tol=1e-8, max_restarts=30)
+    ref = P.gmres_solve(A, b, None, None, params, history=True)
+    got = gmres_solve_slab(A, b, None, None, params, part=part, history=True)
+    assert (got.outer, got.inner, got.converged) == (ref.outer, ref.inner, ref.converged)
+    assert np.linalg.norm(got.x - ref.x) <= 1e-10 * np.linalg.norm(ref.x)
+    x0 = np.random.default_rng(5).standard_normal(b.shape[0])
+    cfg = P.SolverConfig(theta=0.0, theta_amg=0.0, cycle="v", tol=1e-8)
+    B = P.build_cpr(A, cfg)
+    ref = P.gmres_solve(A, b, x0, B, cfg.gmres_params())
+    got = gmres_solve_slab(A, b, x0, B, cfg.gmres_params(), part=part)
+    assert (got.outer, got.inner, got.converged) == (ref.outer, ref.inner, ref.converged)
+    assert np.linalg.norm(got.x - ref.x) <= 1e-10 * np.linalg.norm(ref.x)
+    z = gmres_solve_slab(A, np.zeros_like(b), None, B, cfg.gmres_params(), part=part)
+    assert z.converged and z.inner == 0 and not np.any(z.x)
