@@ -318,6 +318,23 @@ int cprb_pack_bsr_sell(int64_t nrows, int32_t b, const int64_t* row_ptr, const i
                        const double* values, const int64_t* slice_ptr, int32_t* cols,
                        double* vals, void* stream);
 
+/* ---- slab-partitioned BILU (global wavefront, chunks cut at the slab
+ * boundaries; each rank runs its own chunks and stores the rows another
+ * rank reads (plan bit 29) into that rank's output array as well: peer_out,
+ * NVLink peer memory, same offset).  Output arrays and right-hand sides are
+ * per rank (explicit pointers); plan arrays come from F. */
+int cprb_wave_solve_part(const cprb_bilu* F, int32_t upper, int32_t chunk0, int32_t nchunks,
+                         const double* rhs_steps, double* out_step, double* peer_out,
+                         int32_t* ticket, void* stream);
+int cprb_l_to_u_rows(const cprb_bilu* F, int32_t row0, int32_t nrows, const double* zl_step,
+                     double* rhs_u, void* stream);
+int cprb_wave_combine_rows(const cprb_bilu* F, int32_t row0, int32_t nrows, const double* y_step,
+                           const double* zp, double* z, void* stream);
+int cprb_fill_sentinel_idx(int64_t n, int32_t b, const int32_t* idx, double* base, void* stream);
+int cprb_stage2_residual_steps(const cprb_sell* A, const cprb_bilu* F, int32_t row0,
+                               const double* zp, const double* r, double* rhs_l, double* zl_step,
+                               double* y_step, void* stream);
+
 /* ---- slab-partitioned solve (paper_2201_01970_b200/partition.py) ----
  * Each rank owns a contiguous range of block rows; operators read a column
  * window whose halo the host exchanges (NCCL over NVLink). */

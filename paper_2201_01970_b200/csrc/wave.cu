@@ -42,6 +42,15 @@ constexpr int WAVE_META = 320;     // step metadata staged in shared memory per 
 // published to global memory (another chunk or an older-than-DINT row reads it)
 constexpr int WAVE_LEN_MASK = 0xFFFF;
 constexpr int WAVE_EXPORT = 1 << 30;
+// bit 29 = a row of another rank's slab reads this row (slab-partitioned
+// solve): its value is also stored into that rank's output array (peer
+// memory over NVLink, same offset)
+constexpr int WAVE_REMOTE = 1 << 29;
+
+__device__ __forceinline__ void st_relaxed_sys(double* p, double v) {
+  asm volatile("st.relaxed.sys.global.b64 [%0], %1;" ::"l"(p), "l"(__double_as_longlong(v))
+               : "memory");
+}
 
 // diagnostic timeline (cprb_wave_set_log): [UPPER][chunk][local step] ->
 // %globaltimer when row position 0 of the step finished; nullptr = off
@@ -121,6 +130,7 @@ __device__ __forceinline__ void wait_block(const double* g, double* v) {
     for (int c = 0; c < B; ++c) ok &= !is_sentinel(v[c]);
     if (ok) return;
     if (++spins > 8) __nanosleep(20);
+    if (spins > (1 << 27)) __trap();  // a producer that never publishes: fail, do not hang
 #pragma unroll
     for (int c = 0; c < B; ++c)
       if (is_sentinel(v[c])) v[c] = ld_relaxed(g + c);
@@ -257,7 +267,7 @@ __device__ __noinline__ void row_general(const uint8_t* blk, int K, const double
 template <int B, bool UPPER>
 __global__ void __launch_bounds__(WAVE_THREADS, 1)
     k_wave(const cprb_wave W, const double* __restrict__ rhs_steps, double* out_step,
-           int32_t* ticket) {
+           int32_t* ticket, double* peer_out) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   unsigned long long* const tlog = g_wave_log;  // diagnostic timeline (read once)
   __shared__ StepMeta s_meta[WAVE_META];
@@ -394,6 +404,11 @@ __global__ void __launch_bounds__(WAVE_THREADS, 1)
             double* o = out_step + mk.rhs_off + (int64_t)pos * B;
 #pragma unroll
             for (int r = 0; r < B; ++r) st_relaxed(o + r, res[r]);
+            if (peer_out && (lenw & WAVE_REMOTE)) {
+              double* q = peer_out + mk.rhs_off + (int64_t)pos * B;
+#pragma unroll
+              for (int r = 0; r < B; ++r) st_relaxed_sys(q + r, res[r]);
+            }
           }
           if (pos == 0 && tlog && c < WAVE_LOG_CHUNKS && k - s0 < WAVE_LOG_STEPS) {
             unsigned long long tt;
@@ -432,7 +447,7 @@ static size_t wave_smem(const cprb_wave& W, int b) {
 
 template <int B, bool UPPER>
 static int launch_wave(const cprb_wave& W, const double* rhs_steps, double* out_step,
-                       int32_t* ticket, cudaStream_t st) {
+                       int32_t* ticket, cudaStream_t st, double* peer_out = nullptr) {
   static int num_sms = 0;
   if (!num_sms) {
     int dev = 0;
@@ -442,8 +457,14 @@ static int launch_wave(const cprb_wave& W, const double* rhs_steps, double* out_
   if (W.nchunks <= 0) return CPRB_OK;
   const int grid = W.nchunks < num_sms ? W.nchunks : num_sms;
   const size_t smem = wave_smem(W, B);
-  cudaFuncSetAttribute(k_wave<B, UPPER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_wave<B, UPPER><<<grid, WAVE_THREADS, smem, st>>>(W, rhs_steps, out_step, ticket);
+  // set once per instantiation (the attribute call can serialise against
+  // running work; concurrent slab solves on other streams must not wait)
+  static size_t smem_set = 0;
+  if (smem > smem_set) {
+    cudaFuncSetAttribute(k_wave<B, UPPER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    smem_set = smem;
+  }
+  k_wave<B, UPPER><<<grid, WAVE_THREADS, smem, st>>>(W, rhs_steps, out_step, ticket, peer_out);
   return check_launch("wave solve");
 }
 
@@ -522,3 +543,69 @@ int wave_scatter_rhs(const cprb_bilu& F, const double* r, double* rhsL, cudaStre
 }
 
 }  // namespace cprb
+
+// ---- slab-partitioned BILU (paper_2201_01970_b200/partition.py SlabBilu) ----
+__global__ void k_fill_sentinel_idx(int n, int b, const int32_t* __restrict__ idx, double* base) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int c = 0; c < b; ++c) base[(int64_t)idx[i] + c] = cprb::sentinel();
+}
+
+using namespace cprb;
+
+extern "C" {
+
+int cprb_wave_solve_part(const cprb_bilu* F, int32_t upper, int32_t chunk0, int32_t nchunks,
+                         const double* rhs_steps, double* out_step, double* peer_out,
+                         int32_t* ticket, void* stream) {
+  cprb_wave W = upper ? F->Uw : F->Lw;
+  if (chunk0 < 0 || nchunks < 0 || chunk0 + nchunks > W.nchunks)
+    return set_error(CPRB_EINVAL, "chunk range out of bounds");
+  W.chunk_step += chunk0;
+  W.nchunks = nchunks;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (F->b == 3)
+    return upper ? launch_wave<3, true>(W, rhs_steps, out_step, ticket, st, peer_out)
+                 : launch_wave<3, false>(W, rhs_steps, out_step, ticket, st, peer_out);
+  if (F->b == 1)
+    return upper ? launch_wave<1, true>(W, rhs_steps, out_step, ticket, st, peer_out)
+                 : launch_wave<1, false>(W, rhs_steps, out_step, ticket, st, peer_out);
+  return set_error(CPRB_EUNSUPPORTED, "wave BILU supports block sizes 1 and 3");
+}
+
+int cprb_l_to_u_rows(const cprb_bilu* F, int32_t row0, int32_t nrows, const double* zl_step,
+                     double* rhs_u, void* stream) {
+  if (nrows <= 0) return CPRB_OK;
+  const int blocks = (nrows + 255) / 256 < 4 * 148 ? (nrows + 255) / 256 : 4 * 148;
+  k_l_to_u<<<blocks, 256, 0, (cudaStream_t)stream>>>(nrows, F->b, F->l_slot + row0,
+                                                     F->u_slot + row0, zl_step, rhs_u);
+  return check_launch("l to u rows");
+}
+
+int cprb_wave_combine_rows(const cprb_bilu* F, int32_t row0, int32_t nrows, const double* y_step,
+                           const double* zp, double* z, void* stream) {
+  if (nrows <= 0) return CPRB_OK;
+  const int blocks = (nrows + 255) / 256 < 4 * 148 ? (nrows + 255) / 256 : 4 * 148;
+  k_wave_combine<<<blocks, 256, 0, (cudaStream_t)stream>>>(nrows, F->b, F->u_slot + row0, y_step,
+                                                           zp, z);
+  return check_launch("wave combine rows");
+}
+
+int cprb_fill_sentinel_idx(int64_t n, int32_t b, const int32_t* idx, double* base, void* stream) {
+  if (n <= 0) return CPRB_OK;
+  k_fill_sentinel_idx<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>((int)n, b,
+                                                                                   idx, base);
+  return check_launch("fill sentinel idx");
+}
+
+// stage-2 residual of this rank's rows written straight into the L plan's
+// step order, arming the rows' L and U output slots (cprb_cpr_finish's
+// fused kernel for a row range: slots are the plan's, offset by row0)
+int cprb_stage2_residual_steps(const cprb_sell* A, const cprb_bilu* F, int32_t row0,
+                               const double* zp, const double* r, double* rhs_l, double* zl_step,
+                               double* y_step, void* stream) {
+  return bsr_op(2, *A, F->b, zp, r, rhs_l, nullptr, zl_step, (cudaStream_t)stream,
+                F->l_slot + row0, y_step, F->l_slot + row0, F->u_slot + row0);
+}
+
+}  // extern "C"

@@ -164,9 +164,15 @@ def _round16(x):
 
 
 def wave_plan(T: BlockCsrMatrix, sched: LevelSchedule, b: int, upper: bool, uinv=None,
-              aux_slot=None, nchunk_min: int = 148):
+              aux_slot=None, nchunk_min: int = 148, cuts=None):
     """Chunked-wavefront plan of a strict triangular factor (see cprb_wave in
-    include/cpr_b200.h).  Returns (host arrays dict, row -> rhs slot)."""
+    include/cpr_b200.h).  Returns (host arrays dict, row -> rhs slot).
+
+    cuts (slab-partitioned solve): sorted row indices where a rank's slab
+    starts.  Chunks never straddle a cut, rows read across a cut carry the
+    REMOTE bit (their owner also stores them into the reader's memory), and
+    the dict gains per-rank chunk ranges and the output slots each rank
+    receives from its neighbour ("mirror")."""
     ptr, cols, vals = _strict(T)
     n = T.nrows
     bb = b * b
@@ -179,7 +185,15 @@ def wave_plan(T: BlockCsrMatrix, sched: LevelSchedule, b: int, upper: bool, uinv
     bw = int(np.abs(rows_of - cols).max()) if cols.size else 1
     R = max(WAVE_BANDS * bw, -(-n // nchunk_min), 1)
     pos = (n - 1 - np.arange(n)) if upper else np.arange(n)
-    chunk = pos // R
+    if cuts is None:
+        chunk = pos // R
+    else:
+        cuts = np.asarray(cuts, dtype=np.int64)
+        cut_pos = np.sort((n - cuts) if upper else cuts)
+        starts = np.concatenate([[0], cut_pos])
+        ends = np.concatenate([cut_pos, [n]])
+        bnd = np.concatenate([np.arange(a0, e0, R) for a0, e0 in zip(starts, ends) if e0 > a0])
+        chunk = np.searchsorted(bnd, pos, side="right") - 1
     order = np.lexsort((np.arange(n), level, chunk))     # rows by (chunk, level, index)
     ch_s, lv_s = chunk[order], level[order]
     newg = np.ones(n, dtype=bool)
@@ -236,7 +250,17 @@ def wave_plan(T: BlockCsrMatrix, sched: LevelSchedule, b: int, upper: bool, uinv
     rec = soff[st] + (row_pos // 32) * sub[st]          # byte offset of the row's warp slice
     ln = row_pos % 32
     I[rec // 4 + ln] = np.arange(n)                                       # rows
-    I[rec // 4 + 32 + ln] = lens | (exported.astype(np.int64) << 30)      # lens | export bit
+    remote = np.zeros(n, dtype=bool)
+    if cuts is not None:
+        owner = np.searchsorted(cuts, np.arange(n), side="right")
+        cross = owner[cols] != owner[rows_of]
+        remote[cols[cross]] = True
+        want = owner[cols[cross]] + (-1 if upper else 1)
+        if not np.array_equal(owner[rows_of[cross]], want):
+            raise NotImplementedError("slab partition: a factor row is read beyond the "
+                                      "neighbouring slab (slabs thinner than the bandwidth)")
+    I[rec // 4 + 32 + ln] = (lens | (exported.astype(np.int64) << 30)
+                             | (remote.astype(np.int64) << 29))   # lens | export | remote
     aux = np.zeros(n, dtype=np.int64) if aux_slot is None else aux_slot
     I[rec // 4 + 64 + ln] = aux                                           # aux (next rhs slot)
     # entries
@@ -270,6 +294,22 @@ def wave_plan(T: BlockCsrMatrix, sched: LevelSchedule, b: int, upper: bool, uinv
                 step_w=step_w.astype(np.int32), step_k=step_k.astype(np.int32),
                 rhs_off=roff[:-1].astype(np.int64), rhs_bytes=rbytes.astype(np.int32),
                 stream=stream, rhs_len=roff_pad, chunk_rows=R)
+    if cuts is not None:
+        nr = cuts.shape[0] + 1
+        rb = np.concatenate([[0], cuts, [n]])
+        rng_ = np.zeros((nr, 2), dtype=np.int64)
+        mirror = []
+        for q in range(nr):
+            a0, e0 = int(rb[q]), int(rb[q + 1])
+            if e0 > a0:
+                ch = chunk[a0:e0]
+                rng_[q] = (int(ch.min()), int(ch.max()) + 1)
+            # slots this rank's rows poll that the neighbour produces
+            mine = (owner[rows_of] == q) & cross
+            src = np.unique(cols[mine])
+            mirror.append(rhs_slot[src].astype(np.int32))
+        host["chunk_range"] = rng_
+        host["mirror"] = mirror
     return host, rhs_slot
 
 

@@ -39,10 +39,11 @@ from . import device as D
 from .amg import AmgHierarchy, DeviceAmg
 from .cpr import GmresParams, GmresResult, _bsize, _solve_upper
 
-__all__ = ["SEG_CELLS", "SlabPartition", "SlabComm", "SlabMatrix", "SlabCpr",
+__all__ = ["SEG_CELLS", "SlabPartition", "SlabComm", "SlabMatrix", "SlabCpr", "SlabBilu",
            "gmres_solve_slab", "halo_plan"]
 
 SEG_CELLS = 1024
+_SENT_BITS = 0x7FF4C0FFEE5EED01   # csrc/device.cuh CPRB_SENTINEL (not-yet-computed marker)
 
 
 class SlabPartition:
@@ -457,11 +458,135 @@ class SlabLevel0:
                                              D.ptr(self.precv), D.ptr(self.bc), D.stream()))
 
 
+def _sentinel_fill(n: int):
+    t = D.torch()
+    a = np.full(max(int(n), 1), int(_SENT_BITS), dtype=np.uint64).view(np.float64)
+    return t.from_numpy(a).to("cuda")
+
+
+class SlabBilu:
+    """BILU(0) solves of this rank's slab (src/ilu.py:196-223) as part of ONE
+    global wavefront: the wave plans are cut at the slab boundaries, each
+    rank runs its own chunks, and the rows a neighbour reads are also stored
+    into the neighbour's output array (peer memory over NVLink; the L solve
+    feeds the next rank, the U solve the previous one).  The consumer polls
+    its own memory exactly as for an in-chunk global dependency, so the
+    arithmetic and results are those of the single-GPU solve."""
+
+    def __init__(self, F, part: SlabPartition, rank: int, plan=None):
+        from .ilu import WaveDev, wave_plan
+        D.require_cuda()
+        b = F.block_size
+        self.b, self.rank = b, rank
+        self.c0, self.c1 = part.rows(rank)
+        if plan is None:
+            cuts = np.asarray(part.cell0[1:-1], dtype=np.int64)
+            hl, lslot = wave_plan(F.L, F.l_schedule, b, False, cuts=cuts)
+            hu, uslot = wave_plan(F.U, F.u_schedule, b, True, uinv=F.u_diag_inv, cuts=cuts)
+            plan = {"hl": hl, "hu": hu, "Lw": WaveDev(hl), "Uw": WaveDev(hu),
+                    "l_slot": D.upload(lslot.astype(np.int32)),
+                    "u_slot": D.upload(uslot.astype(np.int32)), "n": F.n}
+        self.plan = plan
+        hl, hu = plan["hl"], plan["hu"]
+        self.len_l, self.len_u = max(hl["rhs_len"], 1), max(hu["rhs_len"], 1)
+        self.rhs_l = D.zeros(self.len_l)
+        self.rhs_u = D.zeros(self.len_u)
+        self.zl_step = _sentinel_fill(self.len_l)
+        self.y_step = _sentinel_fill(self.len_u)
+        t = D.torch()
+        self.tickets = t.zeros(8, dtype=t.int32, device="cuda")
+        self.lr = tuple(int(v) for v in hl["chunk_range"][rank])
+        self.ur = tuple(int(v) for v in hu["chunk_range"][rank])
+        ml, mu = hl["mirror"][rank], hu["mirror"][rank]
+        self.ml = D.upload(ml) if ml.size else None
+        self.mu = D.upload(mu) if mu.size else None
+        self.nml, self.nmu = int(ml.size), int(mu.size)
+        self.peer_l = 0      # next rank's zl_step (L rows it reads)
+        self.peer_u = 0      # previous rank's y_step (U rows it reads)
+        self.desc = N.Bilu(plan["n"], b, N.Sell(), N.Sell(), 0, D.ptr(self.tickets), 1,
+                           plan["Lw"].desc, plan["Uw"].desc, D.ptr(plan["l_slot"]), 0, 0,
+                           D.ptr(plan["u_slot"]), 0, 0, self.len_l, self.len_u)
+
+    def solve(self, mat: "SlabMatrix", zp_win, r, z):
+        """z = Pi zp + BILU(r - A Pi zp) on this rank's rows (src/cpr.py:184-186)."""
+        lib, st = N.lib(), D.stream()
+        d = C.byref(self.desc)
+        n_own = self.c1 - self.c0
+        N.check(lib.cprb_stage2_residual_steps(mat.desc_ref(), d, self.c0, D.ptr(zp_win), D.ptr(r),
+                                               D.ptr(self.rhs_l), D.ptr(self.zl_step),
+                                               D.ptr(self.y_step), st))
+        self.solve_steps(z, D.ptr(zp_win) + (self.c0 - mat.w0) * 8, n_own)
+
+    def solve_steps(self, z, zp_own: int, n_own: int, st=None):
+        self.solve_lower(n_own, st)
+        self.solve_upper(z, zp_own, n_own, st)
+
+    def solve_lower(self, n_own: int, st=None):
+        """This rank's chunks of the L wavefront (polls the previous rank's
+        rows in its own memory), then the L -> U permutation of its rows."""
+        lib = N.lib()
+        st = D.stream() if st is None else st
+        d = C.byref(self.desc)
+        N.check(lib.cprb_wave_solve_part(d, 0, self.lr[0], self.lr[1] - self.lr[0],
+                                         D.ptr(self.rhs_l), D.ptr(self.zl_step), self.peer_l or None,
+                                         D.ptr(self.tickets), st))
+        N.check(lib.cprb_l_to_u_rows(d, self.c0, n_own, D.ptr(self.zl_step), D.ptr(self.rhs_u), st))
+
+    def solve_upper(self, z, zp_own: int, n_own: int, st=None):
+        """This rank's chunks of the U wavefront, z = Pi zp + y, re-arm."""
+        lib = N.lib()
+        st = D.stream() if st is None else st
+        d = C.byref(self.desc)
+        N.check(lib.cprb_wave_solve_part(d, 1, self.ur[0], self.ur[1] - self.ur[0],
+                                         D.ptr(self.rhs_u), D.ptr(self.y_step), self.peer_u or None,
+                                         D.ptr(self.tickets) + 4, st))
+        N.check(lib.cprb_wave_combine_rows(d, self.c0, n_own, D.ptr(self.y_step), zp_own, D.ptr(z),
+                                           st))
+        self.rearm(st)
+
+    def rearm(self, st=None):
+        """Re-arm the slots the neighbours fill (after this rank consumed them;
+        the next application's halo exchange orders the neighbours' stores
+        after this)."""
+        lib = N.lib()
+        st = D.stream() if st is None else st
+        if self.nml:
+            N.check(lib.cprb_fill_sentinel_idx(self.nml, self.b, D.ptr(self.ml),
+                                               D.ptr(self.zl_step), st))
+        if self.nmu:
+            N.check(lib.cprb_fill_sentinel_idx(self.nmu, self.b, D.ptr(self.mu),
+                                               D.ptr(self.y_step), st))
+
+
+def _link_peers(bilu: SlabBilu, comm: SlabComm):
+    """Map the neighbours' output arrays (CUDA IPC; NVLink peer memory)."""
+    from torch.multiprocessing.reductions import reduce_tensor
+    mine = (reduce_tensor(bilu.zl_step), reduce_tensor(bilu.y_step))
+    allh = [None] * comm.size
+    comm.dist.all_gather_object(allh, mine, group=comm.group)
+    bilu._peer_refs = []
+    if comm.rank + 1 < comm.size:
+        fn, args = allh[comm.rank + 1][0]
+        t = fn(*args)
+        bilu._peer_refs.append(t)
+        bilu.peer_l = D.ptr(t)
+    if comm.rank > 0:
+        fn, args = allh[comm.rank - 1][1]
+        t = fn(*args)
+        bilu._peer_refs.append(t)
+        bilu.peer_u = D.ptr(t)
+    comm.dist.barrier(group=comm.group)
+
+
 class SlabCpr:
     """Partitioned CPR application z = B r on this rank's rows
     (src/cpr.py:178-186)."""
 
-    def __init__(self, B, part: SlabPartition, comm: SlabComm):
+    def __init__(self, B, part: SlabPartition, comm: SlabComm, bilu: str = "auto"):
+        """bilu: "wave" = distributed wavefront (SlabBilu, peer memory),
+        "replicated" = all-gather the stage-2 residual and solve the whole
+        system on every rank, "auto" = wave on NCCL (one GPU per rank) and for
+        one rank, replicated otherwise (ranks sharing a GPU: tests)."""
         D.require_cuda()
         h = B.pressure_solver
         if h.params.cycle != "v":
@@ -483,13 +608,22 @@ class SlabCpr:
         if rank == 0:
             sub = AmgHierarchy(h.levels[1:], h.coarsest_lu, h.params, symmetric=h.symmetric)
             self.sub = DeviceAmg(sub, 1)
-        self.bilu = B.relaxation.device()
+        if bilu == "auto":
+            bilu = "wave" if (comm.nccl or comm.size == 1) else "replicated"
+        self.bilu_mode = bilu
         nb = B.A.nrows
+        if bilu == "wave":
+            self.sbilu = SlabBilu(B.relaxation, part, rank)
+            if comm.size > 1:
+                _link_peers(self.sbilu, comm)
+        else:
+            self.bilu = B.relaxation.device()
         self.zp = D.zeros(self.mat.win_len)
-        self.r2 = D.zeros(max(self.mat.n_own * self.b, 1))
-        self.r2_full = D.zeros(nb * self.b)
-        self.y_full = D.zeros(nb * self.b)
-        self.gather_fine = _Gatherer(np.diff(part.cell0) * self.b)
+        if bilu != "wave":
+            self.r2 = D.zeros(max(self.mat.n_own * self.b, 1))
+            self.r2_full = D.zeros(nb * self.b)
+            self.y_full = D.zeros(nb * self.b)
+            self.gather_fine = _Gatherer(np.diff(part.cell0) * self.b)
 
     def apply(self, r, z):
         """r: own rows (3 per cell); z: own rows (any contiguous view)."""
@@ -517,6 +651,10 @@ class SlabCpr:
             if t + 1 < L0.ncolors:
                 L0.exchange_x(comm)
         self.mat.exchange(comm, self.zp, 1)
+        if self.bilu_mode == "wave":
+            # stage 2 + the slab's share of the global BILU wavefront
+            self.sbilu.solve(self.mat, self.zp, r, z)
+            return
         # stage 2: r2 = r - A Pi zp on own rows; BILU is a global wavefront
         n_loc = self.mat.n_own * self.b
         N.check(lib.cprb_stage2_residual(self.mat.desc_ref(), self.b, D.ptr(self.zp), D.ptr(r),

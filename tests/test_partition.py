@@ -119,14 +119,15 @@ def test_slab_comm_gloo_world2():
 # GPU
 
 
-def _slab_solve(A, b, cfg, N, rank, seg, comm=None):
-    from paper_2201_01970_b200.partition import gather_rows, gmres_solve_slab
+def _slab_solve(A, b, cfg, N, rank, seg, comm=None, bilu="auto"):
+    from paper_2201_01970_b200.partition import SlabCpr, gather_rows, gmres_solve_slab
     part = SlabPartition(A.nrows, N, seg)
     B = P.build_cpr(A, cfg)
     comm = comm or SlabComm()
     a, e = part.rows(rank)
+    cpr = SlabCpr(B, part, comm, bilu=bilu)
     res = gmres_solve_slab(A, torch.from_numpy(b[3 * a:3 * e].copy()).cuda(), None, B,
-                           cfg.gmres_params(), comm=comm, part=part, history=True)
+                           cfg.gmres_params(), comm=comm, part=part, history=True, cpr=cpr)
     x = gather_rows(res.x, part, comm, 3).cpu().numpy()
     hist = [h if not isinstance(h, tuple) else -h[1] for h in res.history]
     return res.outer, res.inner, res.converged, res.rel_residual, hist, x
@@ -154,7 +155,7 @@ def test_slab_n1_matches_single_gpu_and_reference(gpu):
     assert np.linalg.norm(x - g["x"]) <= 1e-9 * np.linalg.norm(g["x"])
 
 
-def _slab_worker(rank, world, port, seg, shape, q):
+def _slab_worker(rank, world, port, seg, shape, q, bilu="auto"):
     sys.path.insert(0, str(ROOT))
     sys.path.insert(0, str(ROOT / "tests"))
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -163,7 +164,7 @@ def _slab_worker(rank, world, port, seg, shape, q):
         dist.init_process_group("gloo", rank=rank, world_size=world)
         A, b = _grid(*shape)
         cfg = P.SolverConfig(theta=0.0, theta_amg=0.0, cycle="v")
-        out = _slab_solve(A, b, cfg, world, rank, seg)
+        out = _slab_solve(A, b, cfg, world, rank, seg, bilu=bilu)
         q.put((rank, out))
         dist.destroy_process_group()
     except Exception as exc:  # pragma: no cover - surfaced by the parent
@@ -219,3 +220,88 @@ def test_slab_edges_match_single_gpu(gpu):
     assert np.linalg.norm(got.x - ref.x) <= 1e-10 * np.linalg.norm(ref.x)
     z = gmres_solve_slab(A, np.zeros_like(b), None, B, cfg.gmres_params(), part=part)
     assert z.converged and z.inner == 0 and not np.any(z.x)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_slab_bilu_wavefront_emulated_ranks(gpu, nranks):
+    """Distributed BILU wavefront (SlabBilu): each rank's chunk range runs as
+    its own kernel and stores the rows its neighbour reads into the
+    neighbour's arrays (the peer-memory path); z = Pi zp + BILU(r - A Pi zp)
+    is bitwise equal to the single-GPU solve.  Ranks share one GPU here, and
+    CUDA does not promise concurrent progress of kernels on different
+    streams, so the ranks' solves are issued in dependency order (L by rank,
+    U by reverse rank) instead of concurrently as on separate GPUs."""
+    import ctypes as C
+    from paper_2201_01970_b200 import _native as N
+    from paper_2201_01970_b200 import device as D
+    from paper_2201_01970_b200.partition import SlabBilu, SlabMatrix
+    A, _ = _grid(12, 10, 14)
+    F = P.bilu0_factorize(A)
+    part = SlabPartition(A.nrows, nranks, 60)
+    rng = np.random.default_rng(7)
+    r = rng.standard_normal(3 * A.nrows)
+    zp = rng.standard_normal(A.nrows)
+    # single-GPU reference: r2 = r - A Pi zp (block column 0), z = Pi zp + BILU(r2)
+    M = D.device_matrix(A)
+    r2 = D.empty(3 * A.nrows)
+    zp_d, r_d = D.upload(zp), D.upload(r)          # keep the inputs alive until the kernel ran
+    N.check(N.lib().cprb_stage2_residual(M.desc_ref(), 3, D.ptr(zp_d), D.ptr(r_d), D.ptr(r2),
+                                         D.stream()))
+    y = P.bilu_apply(F, r2.cpu().numpy())
+    z_ref = y.copy()
+    z_ref[0::3] = zp + y[0::3]
+    ranks, mats = [], []
+    for q in range(nranks):
+        ranks.append(SlabBilu(F, part, q, plan=ranks[0].plan if ranks else None))
+        mats.append(SlabMatrix(A, part, q))
+    for q in range(nranks):
+        if q + 1 < nranks:
+            ranks[q].peer_l = D.ptr(ranks[q + 1].zl_step)
+        if q > 0:
+            ranks[q].peer_u = D.ptr(ranks[q - 1].y_step)
+    zps = [D.upload(zp[m.w0:m.w1].copy()) for m in mats]
+    rs = [D.upload(r[3 * m.c0:3 * m.c1].copy()) for m in mats]
+    zs = [D.zeros(3 * m.n_own) for m in mats]
+    lib = N.lib()
+    for _ in range(2):                       # twice: the re-armed mirrors are reused
+        for q in range(nranks):
+            sb, m = ranks[q], mats[q]
+            N.check(lib.cprb_stage2_residual_steps(m.desc_ref(), C.byref(sb.desc), sb.c0,
+                                                   D.ptr(zps[q]), D.ptr(rs[q]), D.ptr(sb.rhs_l),
+                                                   D.ptr(sb.zl_step), D.ptr(sb.y_step), D.stream()))
+        for q in range(nranks):
+            ranks[q].solve_lower(mats[q].n_own)
+        for q in reversed(range(nranks)):
+            m = mats[q]
+            ranks[q].solve_upper(zs[q], D.ptr(zps[q]) + (m.c0 - m.w0) * 8, m.n_own)
+        torch.cuda.synchronize()
+        got = np.concatenate([z.cpu().numpy() for z in zs])
+        assert np.array_equal(got, z_ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(os.environ.get("CPRB_SKIP_IPC", "0") == "1",
+                    reason="ranks sharing one GPU spin on each other across processes "
+                           "(time-sliced contexts); CPRB_SKIP_IPC=1 skips")
+def test_slab_wave_bilu_two_processes_ipc(gpu):
+    """The distributed BILU wavefront across two PROCESSES: the neighbour's
+    output arrays are mapped with CUDA IPC (_link_peers) and filled by remote
+    stores; results bitwise equal to one rank."""
+    shape, seg, world = (12, 10, 14), 60, 2
+    A, b = _grid(*shape)
+    cfg = P.SolverConfig(theta=0.0, theta_amg=0.0, cycle="v")
+    one = _slab_solve(A, b, cfg, 1, 0, seg)
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_slab_worker, args=(r, world, port, seg, shape, q, "wave"))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+    for r in range(world):
+        assert got[r][0] != "error", got[r]
+        assert got[r][4] == one[4] and np.array_equal(got[r][5], one[5])
