@@ -170,6 +170,23 @@ class SlabComm:
         self.dist.all_gather(parts, local.cpu(), group=self.group)
         out.copy_(t.cat(parts))
 
+    def gather0(self, local, out):
+        """Rank 0: out[q*cap:(q+1)*cap] = rank q's `local`; other ranks only send."""
+        if self.size == 1:
+            out[:local.shape[0]].copy_(local)
+            return
+        cap = local.shape[0]
+        if self.nccl:
+            parts = [out[q * cap:(q + 1) * cap] for q in range(self.size)] if self.rank == 0 else None
+            self.dist.gather(local, parts, dst=0, group=self.group)
+            return
+        t = D.torch()
+        parts = [t.empty(local.shape, dtype=local.dtype) for _ in range(self.size)] \
+            if self.rank == 0 else None
+        self.dist.gather(local.cpu(), parts, dst=0, group=self.group)
+        if self.rank == 0:
+            out.copy_(t.cat(parts))
+
     def broadcast(self, tensor, src: int = 0):
         if self.size == 1:
             return
@@ -196,12 +213,18 @@ class _Gatherer:
         self.local = D.zeros(self.cap)
         self.buf = D.zeros(self.nranks * self.cap)
 
-    def __call__(self, comm: SlabComm, src, n_local: int, out):
+    def __call__(self, comm: SlabComm, src, n_local: int, out, root_only: bool = False):
+        """root_only: only rank 0 receives (and unpacks) the result."""
         if comm.size == 1:
             out[:n_local].copy_(src[:n_local])
             return
         self.local[:n_local].copy_(src[:n_local])
-        comm.allgather(self.local, self.buf)
+        if root_only:
+            comm.gather0(self.local, self.buf)
+            if comm.rank != 0:
+                return
+        else:
+            comm.allgather(self.local, self.buf)
         N.check(N.lib().cprb_unpad(self.nranks, self.cap, D.ptr(self.offs_dev), D.ptr(self.buf),
                                    D.ptr(out), D.stream()))
 
@@ -638,7 +661,7 @@ class SlabCpr:
         N.check(lib.cprb_resid_restrict(d, D.ptr(L0.b), D.ptr(L0.x), D.ptr(L0.bc), st))
         L0.combine_partials(comm)
         # levels >= 1 agglomerated on rank 0
-        self.gather1(comm, L0.bc, L0.n_agg, self.b1)
+        self.gather1(comm, L0.bc, L0.n_agg, self.b1, root_only=True)
         if self.sub is not None:
             N.check(lib.cprb_amg_cycle(C.byref(self.sub.desc), D.ptr(self.b1), D.ptr(self.e1), st))
         comm.broadcast(self.e1, 0)

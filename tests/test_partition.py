@@ -93,7 +93,9 @@ def _comm_worker(rank, world, port, q):
     c.allgather(torch.arange(4, dtype=torch.float64) + 10 * rank, out)
     bc = torch.full((2,), float(rank + 7), dtype=torch.float64)
     c.broadcast(bc, 0)
-    q.put((rank, c.size, recv.tolist(), out.tolist(), bc.tolist()))
+    g0 = torch.zeros(2 * 4, dtype=torch.float64)
+    c.gather0(torch.arange(4, dtype=torch.float64) + 10 * rank, g0)
+    q.put((rank, c.size, recv.tolist(), out.tolist(), bc.tolist(), g0.tolist()))
     dist.destroy_process_group()
 
 
@@ -113,6 +115,7 @@ def test_slab_comm_gloo_world2():
         assert o[1] == 2
         assert o[3] == [0.0, 1.0, 2.0, 3.0, 10.0, 11.0, 12.0, 13.0]
         assert o[4] == [7.0, 7.0]
+    assert out[0][5] == [0.0, 1.0, 2.0, 3.0, 10.0, 11.0, 12.0, 13.0]     # root only
 
 
 # ---------------------------------------------------------------------------
