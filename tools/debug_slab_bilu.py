@@ -76,90 +76,3 @@ N.check(lib.cprb_wave_solve_part(C.byref(sb.desc), 1, sb.ur[0], sb.ur[1] - sb.ur
 torch.cuda.synchronize()
 print("rank0 U done")
 
-# ---- concurrency probe: rank 1's L (needs rank 0) first, then rank 0's L
-import time  # noqa: E402
-for q in range(nr):
-    sb, m = ranks[q], mats[q]
-    N.check(lib.cprb_stage2_residual_steps(m.desc_ref(), C.byref(sb.desc), sb.c0, D.ptr(zps[q]),
-                                           D.ptr(rs[q]), D.ptr(sb.rhs_l), D.ptr(sb.zl_step),
-                                           D.ptr(sb.y_step), st))
-for q in range(nr):
-    ranks[q].rearm(st)
-torch.cuda.synchronize()
-s0, s1 = torch.cuda.Stream(), torch.cuda.Stream()
-print("L mirror r1 armed", sentinels(ranks[1].zl_step, hl["mirror"][1], 3), flush=True)
-sb = ranks[1]
-N.check(lib.cprb_wave_solve_part(C.byref(sb.desc), 0, sb.lr[0], sb.lr[1] - sb.lr[0], D.ptr(sb.rhs_l),
-                                 D.ptr(sb.zl_step), None, D.ptr(sb.tickets), s1.cuda_stream))
-time.sleep(0.5)
-print("after 0.5 s: s1 done?", s1.query(), flush=True)
-sb = ranks[0]
-N.check(lib.cprb_wave_solve_part(C.byref(sb.desc), 0, sb.lr[0], sb.lr[1] - sb.lr[0], D.ptr(sb.rhs_l),
-                                 D.ptr(sb.zl_step), sb.peer_l or None, D.ptr(sb.tickets), s0.cuda_stream))
-t0 = time.time()
-while time.time() - t0 < 5 and not (s0.query() and s1.query()):
-    time.sleep(0.2)
-print("s0 done", s0.query(), "s1 done", s1.query(), flush=True)
-
-# ---- full concurrent pipeline with per-stage events
-for q in range(nr):
-    sb, m = ranks[q], mats[q]
-    N.check(lib.cprb_stage2_residual_steps(m.desc_ref(), C.byref(sb.desc), sb.c0, D.ptr(zps[q]),
-                                           D.ptr(rs[q]), D.ptr(sb.rhs_l), D.ptr(sb.zl_step),
-                                           D.ptr(sb.y_step), st))
-for q in range(nr):
-    ranks[q].rearm(st)
-torch.cuda.synchronize()
-streams = [torch.cuda.Stream() for _ in range(nr)]
-ev = {}
-zs = [D.zeros(3 * m.n_own) for m in mats]
-for q in range(nr):
-    sb, m = ranks[q], mats[q]
-    s_ = streams[q].cuda_stream
-    d = C.byref(sb.desc)
-    N.check(lib.cprb_wave_solve_part(d, 0, sb.lr[0], sb.lr[1] - sb.lr[0], D.ptr(sb.rhs_l),
-                                     D.ptr(sb.zl_step), sb.peer_l or None, D.ptr(sb.tickets), s_))
-    e = torch.cuda.Event(); e.record(streams[q]); ev[(q, "L")] = e
-    N.check(lib.cprb_l_to_u_rows(d, sb.c0, m.n_own, D.ptr(sb.zl_step), D.ptr(sb.rhs_u), s_))
-    e = torch.cuda.Event(); e.record(streams[q]); ev[(q, "l2u")] = e
-    N.check(lib.cprb_wave_solve_part(d, 1, sb.ur[0], sb.ur[1] - sb.ur[0], D.ptr(sb.rhs_u),
-                                     D.ptr(sb.y_step), sb.peer_u or None, D.ptr(sb.tickets) + 4, s_))
-    e = torch.cuda.Event(); e.record(streams[q]); ev[(q, "U")] = e
-t0 = time.time()
-while time.time() - t0 < 5 and not all(e.query() for e in ev.values()):
-    time.sleep(0.2)
-print({f"{k[0]}{k[1]}": e.query() for k, e in ev.items()}, flush=True)
-
-# ---- bisect: full solve_steps per rank (L, l2u, U, combine, rearm)
-for variant in ("combine", "solve_steps"):
-    for q in range(nr):
-        sb, m = ranks[q], mats[q]
-        N.check(lib.cprb_stage2_residual_steps(m.desc_ref(), C.byref(sb.desc), sb.c0, D.ptr(zps[q]),
-                                               D.ptr(rs[q]), D.ptr(sb.rhs_l), D.ptr(sb.zl_step),
-                                               D.ptr(sb.y_step), st))
-    for q in range(nr):
-        ranks[q].rearm(st)
-    torch.cuda.synchronize()
-    streams = [torch.cuda.Stream() for _ in range(nr)]
-    evs = []
-    for q in range(nr):
-        sb, m = ranks[q], mats[q]
-        s_ = streams[q].cuda_stream
-        zp_own = D.ptr(zps[q]) + (m.c0 - m.w0) * 8
-        if variant == "solve_steps":
-            sb.solve_steps(zs[q], zp_own, m.n_own, st=s_)
-        else:
-            d = C.byref(sb.desc)
-            N.check(lib.cprb_wave_solve_part(d, 0, sb.lr[0], sb.lr[1] - sb.lr[0], D.ptr(sb.rhs_l),
-                                             D.ptr(sb.zl_step), sb.peer_l or None, D.ptr(sb.tickets), s_))
-            N.check(lib.cprb_l_to_u_rows(d, sb.c0, m.n_own, D.ptr(sb.zl_step), D.ptr(sb.rhs_u), s_))
-            N.check(lib.cprb_wave_solve_part(d, 1, sb.ur[0], sb.ur[1] - sb.ur[0], D.ptr(sb.rhs_u),
-                                             D.ptr(sb.y_step), sb.peer_u or None, D.ptr(sb.tickets) + 4, s_))
-            N.check(lib.cprb_wave_combine_rows(d, sb.c0, m.n_own, D.ptr(sb.y_step), zp_own, D.ptr(zs[q]), s_))
-        e = torch.cuda.Event(); e.record(streams[q]); evs.append(e)
-    t0 = time.time()
-    while time.time() - t0 < 5 and not all(e.query() for e in evs):
-        time.sleep(0.2)
-    print(variant, [e.query() for e in evs], flush=True)
-    if not all(e.query() for e in evs):
-        break
