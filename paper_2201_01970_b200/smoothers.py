@@ -65,7 +65,9 @@ class ScalarSplit:
         vals = np.asarray(A.values, dtype=np.float64)
         rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(ptr))
         pr, pc = inv[rows], inv[cols]
-        order = np.lexsort((pc, pr))            # A.permuted(perm): sorted permuted columns
+        # A.permuted(perm): rows by permuted index, sorted permuted columns
+        # ((row, col) pairs are unique, so one integer key sorts them)
+        order = np.argsort(pr * max(n, 1) + pc)
         pr, pc, pv = pr[order], pc[order], vals[order]
         off = pr != pc
         diag = np.zeros(n)
@@ -78,8 +80,7 @@ class ScalarSplit:
         self.off_cols = pc[off]
         self.off_vals = pv[off]
         self.off_ptr = np.zeros(n + 1, dtype=np.int64)
-        np.add.at(self.off_ptr[1:], self.off_rows, 1)
-        np.cumsum(self.off_ptr, out=self.off_ptr)
+        np.cumsum(np.bincount(self.off_rows, minlength=n), out=self.off_ptr[1:])
         sizes = np.array([g.shape[0] for g in partition.groups], dtype=np.int64)
         self.color_rows = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
         self.ncolors = len(partition.groups)
@@ -110,8 +111,7 @@ class ScalarSplit:
         ent_cols = self.off_cols
         ent_vals = self.off_vals
         lo_cnt = (self.off_cols < row_color_start[self.off_rows])
-        lo_per_row = np.zeros(self.n, dtype=np.int64)
-        np.add.at(lo_per_row, self.off_rows[lo_cnt], 1)
+        lo_per_row = np.bincount(self.off_rows[lo_cnt], minlength=self.n).astype(np.int64)
         lane_lo = np.zeros(L, dtype=np.int32)
         lane_lo[real] = lo_per_row[lane_row[real]]
         h = D.pack_sell(lane_row, lane_ptr, ent_cols, ent_vals, 1, self.n, lane_len_lo=lane_lo)
