@@ -325,23 +325,32 @@ class WaveDev:
 
 
 class DeviceBilu:
-    """Level-ordered SELL-32 copies of the strict L and U factors."""
+    """Device plan of the BILU(0) solves: chunked-wavefront plans (default) or
+    level-ordered SELL-32 copies of the strict factors (use_wave=False)."""
 
     def __init__(self, F: BiluFactors, use_wave: bool = True):
         D.require_cuda()
         b = F.block_size
         if b not in (1, 3):
             raise NotImplementedError(f"device BILU supports block sizes 1 and 3, got {b}")
-        hl, _ = _level_sell(F.L, F.l_schedule, b)
-        hu, ui = _level_sell(F.U, F.u_schedule, b, F.u_diag_inv)
-        self.L = D.SellDev(hl)
-        self.U = D.SellDev(hu)
-        self.uinv = D.upload(ui)
+        self.use_wave = bool(F.n > 0 and use_wave)
+        if self.use_wave:
+            # the wave plans carry their own copies of the factors; the
+            # level-ordered SELL-32 layout is only built for the sync-free variant
+            self.L = self.U = self.uinv = None
+            ldesc = udesc = N.Sell()
+            uptr = 0
+        else:
+            hl, _ = _level_sell(F.L, F.l_schedule, b)
+            hu, ui = _level_sell(F.U, F.u_schedule, b, F.u_diag_inv)
+            self.L = D.SellDev(hl)
+            self.U = D.SellDev(hu)
+            self.uinv = D.upload(ui)
+            ldesc, udesc, uptr = self.L.desc, self.U.desc, D.ptr(self.uinv)
         t = D.torch()
         self.tickets = t.zeros(8, dtype=t.int32, device="cuda")
         self.work = D.empty(max(F.n * b, 1))
         self.n, self.b = F.n, b
-        self.use_wave = bool(F.n > 0 and use_wave)
         if self.use_wave:
             hu, uslot = wave_plan(F.U, F.u_schedule, b, True, uinv=F.u_diag_inv)
             hl, lslot = wave_plan(F.L, F.l_schedule, b, False)
@@ -359,7 +368,7 @@ class DeviceBilu:
         else:
             wl, wu = N.Wave(), N.Wave()
             extra = (0, 0, 0, 0, 0, 0, 0, 0)
-        self.desc = N.Bilu(F.n, b, self.L.desc, self.U.desc, D.ptr(self.uinv), D.ptr(self.tickets),
+        self.desc = N.Bilu(F.n, b, ldesc, udesc, uptr, D.ptr(self.tickets),
                            1 if self.use_wave else 0, wl, wu, *extra)
 
     def apply(self, r, z):
