@@ -71,7 +71,15 @@ class Clocks:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def mark(self, start: bool):
+        """Bracket the timed region (samples outside it are not reported)."""
+        if start:
+            self.t0 = time.time()
+        else:
+            self.t1 = time.time()
+            time.sleep(0.05)        # let the sample covering the end arrive
 
     def __exit__(self, *a):
         if self.proc is not None:
@@ -84,7 +92,10 @@ class Clocks:
     def summary(self):
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        t0, t1 = getattr(self, "t0", None), getattr(self, "t1", None)
+        lines = [ln for t, ln in self.lines
+                 if t0 is None or t1 is None or (t0 <= t <= t1 + 0.025)]
+        for ln in lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 8:
                 continue
@@ -190,6 +201,7 @@ def run_ours(args):
     def solve():
         return P.gmres_solve(A, bd, None, B, params)
 
+    clk = Clocks(local).__enter__()     # sampler up before the timed region
     for _ in range(args.warmup):
         res = solve()
     torch.cuda.synchronize()
@@ -198,13 +210,15 @@ def run_ours(args):
     st = torch.cuda.current_stream()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    with Clocks(local) as clk:
-        torch.cuda.synchronize()
-        e0.record(st)
-        for _ in range(args.steps):
-            res = solve()
-        e1.record(st)
-        torch.cuda.synchronize()
+    torch.cuda.synchronize()
+    clk.mark(True)
+    e0.record(st)
+    for _ in range(args.steps):
+        res = solve()
+    e1.record(st)
+    torch.cuda.synchronize()
+    clk.mark(False)
+    clk.__exit__()
     ms = e0.elapsed_time(e1) / args.steps
     if ws > 1:
         ms = max_over_ranks(ms, dist, torch, "cuda")
@@ -348,6 +362,7 @@ def run_partitioned(args):
     def solve(rhs):
         return S.gmres_solve_slab(A, rhs, None, B, params, comm=comm, part=part, cpr=cpr)
 
+    clk = Clocks(local).__enter__()     # sampler up before the timed region
     for _ in range(args.warmup):
         res = solve(bd)
     torch.cuda.synchronize()
@@ -356,13 +371,15 @@ def run_partitioned(args):
     st = torch.cuda.current_stream()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    with Clocks(local) as clk:
-        torch.cuda.synchronize()
-        e0.record(st)
-        for _ in range(args.steps):
-            res = solve(bd)
-        e1.record(st)
-        torch.cuda.synchronize()
+    torch.cuda.synchronize()
+    clk.mark(True)
+    e0.record(st)
+    for _ in range(args.steps):
+        res = solve(bd)
+    e1.record(st)
+    torch.cuda.synchronize()
+    clk.mark(False)
+    clk.__exit__()
     ms = e0.elapsed_time(e1) / args.steps
     if ws > 1:
         ms = max_over_ranks(ms, dist, torch, "cuda")
