@@ -308,3 +308,31 @@ def test_slab_wave_bilu_two_processes_ipc(gpu):
     for r in range(world):
         assert got[r][0] != "error", got[r]
         assert got[r][4] == one[4] and np.array_equal(got[r][5], one[5])
+
+
+@pytest.mark.parametrize("N", [2, 3])
+def test_wave_plan_cuts(N):
+    """Host side of the distributed BILU wavefront: chunks never straddle a
+    slab boundary, each rank owns a contiguous chunk range in wavefront
+    order, rows read across a boundary carry the REMOTE bit, and the mirror
+    slots a rank re-arms are exactly the neighbour rows its rows read."""
+    from paper_2201_01970_b200.ilu import _strict, wave_plan
+    A, _ = _grid(12, 10, 14)
+    F = P.bilu0_factorize(A)
+    part = SlabPartition(A.nrows, N, 60)
+    cuts = np.asarray(part.cell0[1:-1], dtype=np.int64)
+    for upper, T, S in ((False, F.L, F.l_schedule), (True, F.U, F.u_schedule)):
+        h, slot = wave_plan(T, S, 3, upper, uinv=F.u_diag_inv if upper else None, cuts=cuts)
+        rng_ = h["chunk_range"]
+        order = list(range(N))[::-1] if upper else list(range(N))
+        assert rng_[order[0]][0] == 0 and rng_[order[-1]][1] == h["nchunks"]
+        for a, b in zip(order, order[1:]):
+            assert rng_[a][1] == rng_[b][0]                 # contiguous, wavefront order
+        ptr, cols, _ = _strict(T)
+        rows = np.repeat(np.arange(T.nrows), np.diff(ptr))
+        owner = part.owner(np.arange(T.nrows))
+        cross = owner[cols] != owner[rows]
+        for q in range(N):
+            want = np.unique(slot[np.unique(cols[cross & (owner[rows] == q)])])
+            assert np.array_equal(np.sort(h["mirror"][q]), want)
+        assert cross.any()
