@@ -602,11 +602,11 @@ class DeviceAmg:
 
     # -- K-cycle on the device (csrc/kcycle.cu): no host synchronisation ---------
     def kdesc(self):
-        """Descriptor of the device K-cycle (FCG flavour), or None when the
-        host-driven path is required (FGMRES flavour, CPRB_HOST_KCYCLE=1)."""
+        """Descriptor of the device K-cycle (FCG or FGMRES flavour), or None
+        when the host-driven path is requested (CPRB_HOST_KCYCLE=1)."""
         if getattr(self, "_kdesc", None) is not None:
             return self._kdesc
-        if not self.desc.use_fcg or os.environ.get("CPRB_HOST_KCYCLE", "0") == "1":
+        if os.environ.get("CPRB_HOST_KCYCLE", "0") == "1":
             return None
         L = self.nlevels
         arr = (N.Sell * max(L - 1, 1))()

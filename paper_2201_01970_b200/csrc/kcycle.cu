@@ -87,6 +87,87 @@ __global__ void k_kdense(int n, const double* __restrict__ inv, const double* __
 }
 
 // grid for the grid-stride kernels (axpys)
+// ---- flexible GMRES flavour (src/amg.py:199-225), two steps ----------------
+enum { G_ACTIVE = 0, G_BETA = 1, G_H00 = 2, G_H10 = 3, G_H01 = 4, G_H11 = 5, G_H21 = 6,
+       G_CONT = 7, G_Y0 = 8, G_Y1 = 9, G_MEFF = 10, G_T = 11, G_NS = 16 };
+
+// beta = sqrt(s[G_T]); active = beta != 0
+__global__ void k_fg_beta(double* s) {
+  s[G_BETA] = sqrt(s[G_T]);
+  s[G_ACTIVE] = (s[G_BETA] != 0.0) ? 1.0 : 0.0;
+}
+
+// s[dst] = sqrt(s[G_T]); the next Arnoldi step runs iff it is nonzero
+__global__ void k_fg_norm(double* s, int dst) {
+  s[dst] = sqrt(s[G_T]);
+  s[G_CONT] = (s[G_ACTIVE] != 0.0 && s[dst] != 0.0) ? 1.0 : 0.0;
+}
+
+// out = x / s[idx]  while s[flag] != 0
+__global__ void k_div_pred(int n, const double* __restrict__ s, int idx, int flag,
+                           const double* __restrict__ x, double* __restrict__ out) {
+  if (s[flag] == 0.0) return;
+  const double h = s[idx];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = x[i] / h;
+}
+
+// out = (sign * s[idx]) * x + y  while s[flag] != 0
+__global__ void k_axpy_s(int n, const double* __restrict__ s, int idx, int flag, double sign,
+                         const double* __restrict__ x, const double* y, double* out) {
+  if (s[flag] == 0.0) return;
+  const double a = sign * s[idx];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = a * x[i] + y[i];
+}
+
+__global__ void k_fg_restore(double* s) {
+  s[G_CONT] = (s[G_ACTIVE] != 0.0 && s[G_H10] != 0.0) ? 1.0 : 0.0;
+}
+
+// least squares min || H y - beta e1 || for m_eff = 1 or 2 (Givens QR of the
+// (m_eff+1) x m_eff Hessenberg matrix; np.linalg.lstsq in the reference,
+// equal up to rounding for full column rank)
+__global__ void k_fg_lstsq(double* s) {
+  s[G_Y0] = 0.0;
+  s[G_Y1] = 0.0;
+  if (s[G_ACTIVE] == 0.0) {
+    s[G_MEFF] = 0.0;
+    return;
+  }
+  const int m = s[G_CONT] != 0.0 ? 2 : 1;
+  s[G_MEFF] = m;
+  double r00 = s[G_H00], r10 = s[G_H10], r01 = s[G_H01], r11 = s[G_H11], r21 = s[G_H21];
+  double g0 = s[G_BETA], g1 = 0.0, g2 = 0.0;
+  double d = hypot(r00, r10);
+  if (d == 0.0) return;
+  double c = r00 / d, sn = r10 / d;
+  r00 = d;
+  const double t01 = c * r01 + sn * r11;
+  r11 = -sn * r01 + c * r11;
+  r01 = t01;
+  g1 = -sn * g0;
+  g0 = c * g0;
+  if (m == 1) {
+    s[G_Y0] = g0 / r00;
+    return;
+  }
+  d = hypot(r11, r21);
+  if (d == 0.0) {
+    s[G_Y0] = g0 / r00;
+    return;
+  }
+  c = r11 / d;
+  sn = r21 / d;
+  r11 = d;
+  g2 = -sn * g1;
+  g1 = c * g1;
+  (void)g2;
+  const double y1 = g1 / r11;
+  s[G_Y1] = y1;
+  s[G_Y0] = (g0 - r01 * y1) / r00;
+}
+
 static inline int kb(int64_t n) {
   int64_t g = (n + 255) / 256;
   if (g > 148 * 8) g = 148 * 8;
@@ -129,6 +210,8 @@ static int kdot(const KPlan& P, int n, const double* x, const double* y, double*
 
 static int kcycle_at(const KPlan& P, const cprb_amg& h, int l, const double* b, double* x,
                      cudaStream_t st);
+static int fgmres_at(const KPlan& P, const cprb_amg& h, int l, const double* rhs,
+                     cudaStream_t st);
 
 // two flexible-CG steps at level l with the cycle at l as preconditioner;
 // the result is P.x[l]
@@ -165,6 +248,44 @@ static int fcg_at(const KPlan& P, const cprb_amg& h, int l, const double* rhs, c
   return check_launch("fcg");
 }
 
+// two flexible-GMRES steps at level l (src/amg.py:199-225); result P.x[l]
+static int fgmres_at(const KPlan& P, const cprb_amg& h, int l, const double* rhs,
+                     cudaStream_t st) {
+  const int n = P.n[l];
+  double* s = P.s[l];
+  double *x = P.x[l], *v0 = P.r[l], *z0 = P.z1[l], *w = P.ap1[l], *z1 = P.z2[l];
+  double *v1 = P.p2[l], *w1 = P.ap2[l];
+  int rc;
+  cudaMemsetAsync(x, 0, sizeof(double) * n, st);
+  if ((rc = kdot(P, n, rhs, rhs, s + G_T, st))) return rc;
+  k_fg_beta<<<1, 1, 0, st>>>(s);
+  k_div_pred<<<kb(n), 256, 0, st>>>(n, s, G_BETA, G_ACTIVE, rhs, v0);
+  // j = 0
+  if ((rc = kcycle_at(P, h, l, v0, z0, st))) return rc;
+  if ((rc = bsr_op(0, P.spmv[l], 1, z0, nullptr, w, nullptr, nullptr, st))) return rc;
+  if ((rc = kdot(P, n, w, v0, s + G_H00, st))) return rc;
+  k_axpy_s<<<kb(n), 256, 0, st>>>(n, s, G_H00, G_ACTIVE, -1.0, v0, w, w);
+  if ((rc = kdot(P, n, w, w, s + G_T, st))) return rc;
+  k_fg_norm<<<1, 1, 0, st>>>(s, G_H10);
+  k_div_pred<<<kb(n), 256, 0, st>>>(n, s, G_H10, G_CONT, w, v1);
+  // j = 1 (skipped by predicate after a happy breakdown)
+  if ((rc = kcycle_at(P, h, l, v1, z1, st))) return rc;
+  if ((rc = bsr_op(0, P.spmv[l], 1, z1, nullptr, w1, nullptr, nullptr, st))) return rc;
+  if ((rc = kdot(P, n, w1, v0, s + G_H01, st))) return rc;
+  k_axpy_s<<<kb(n), 256, 0, st>>>(n, s, G_H01, G_CONT, -1.0, v0, w1, w1);
+  if ((rc = kdot(P, n, w1, v1, s + G_H11, st))) return rc;
+  k_axpy_s<<<kb(n), 256, 0, st>>>(n, s, G_H11, G_CONT, -1.0, v1, w1, w1);
+  if ((rc = kdot(P, n, w1, w1, s + G_T, st))) return rc;
+  k_fg_norm<<<1, 1, 0, st>>>(s, G_H21);
+  // k_fg_norm cleared G_CONT when H21 == 0; m_eff is 2 either way
+  // (src/amg.py:216-218), so restore it from H10 before the solve
+  k_fg_restore<<<1, 1, 0, st>>>(s);
+  k_fg_lstsq<<<1, 1, 0, st>>>(s);
+  k_axpy_s<<<kb(n), 256, 0, st>>>(n, s, G_Y0, G_ACTIVE, 1.0, z0, x, x);
+  k_axpy_s<<<kb(n), 256, 0, st>>>(n, s, G_Y1, G_CONT, 1.0, z1, x, x);
+  return check_launch("fgmres");
+}
+
 // src/amg.py:245-267 (K): x = cycle_l(b) from a zero guess
 static int kcycle_at(const KPlan& P, const cprb_amg& h, int l, const double* b, double* x,
                      cudaStream_t st) {
@@ -185,7 +306,8 @@ static int kcycle_at(const KPlan& P, const cprb_amg& h, int l, const double* b, 
                                                            P.coarse_x);
     ec = P.coarse_x;
   } else {
-    if ((rc = fcg_at(P, h, l + 1, bc, st))) return rc;
+    if ((rc = (h.use_fcg ? fcg_at(P, h, l + 1, bc, st) : fgmres_at(P, h, l + 1, bc, st))))
+      return rc;
     ec = P.x[l + 1];
   }
   k_kprolong<<<kfull(Lv.n), 256, 0, st>>>(Lv.n, Lv.aggp, ec, x);
@@ -219,7 +341,6 @@ extern "C" {
 int cprb_kcycle_create(const cprb_amg* h, const cprb_sell* level_spmv, int32_t pre_sweeps,
                        int32_t post_sweeps, void** out) {
   if (!h || !out) return set_error(CPRB_EINVAL, "null argument");
-  if (!h->use_fcg) return set_error(CPRB_EUNSUPPORTED, "device K-cycle implements the FCG flavour");
   auto* P = new KPlan();
   const int L = h->nlevels;
   P->nl = L;
@@ -237,7 +358,7 @@ int cprb_kcycle_create(const cprb_amg* h, const cprb_sell* level_spmv, int32_t p
     if (l >= 1 && l < L - 1) {
       P->x[l] = P->alloc(n); P->r[l] = P->alloc(n); P->z1[l] = P->alloc(n);
       P->ap1[l] = P->alloc(n); P->z2[l] = P->alloc(n); P->p2[l] = P->alloc(n);
-      P->ap2[l] = P->alloc(n); P->s[l] = P->alloc(S_NS);
+      P->ap2[l] = P->alloc(n); P->s[l] = P->alloc(G_NS);
     }
     if (l < L - 1) P->rc[l] = P->alloc((size_t)P->n[l + 1]);
   }

@@ -277,6 +277,23 @@ def test_device_kcycle_bitwise_equals_host_kcycle(gpu):
         assert np.array_equal(z_host.cpu().numpy(), z_dev.cpu().numpy())
 
 
+def test_device_kcycle_fgmres_flavour_matches_host(gpu):
+    """FGMRES flavour (non-symmetric pressure operators, src/amg.py:199-225)
+    of the device K-cycle against the host-driven one: equal up to the small
+    least-squares solve (Givens QR on the device, LAPACK lstsq on the host)."""
+    from paper_2201_01970_b200 import device as D
+    (M, _), = P.generate_blackoil_like_sequence(24, 20, 12, 1, 0.01, 4).systems
+    params = P.AmgParams(theta_amg=0.0, cycle="k", krylov="fgmres")
+    h = P.build_hierarchy(P.pressure_matrix(M), params)
+    dev = h.device(1)
+    assert not dev.desc.use_fcg and dev.kdesc() is not None
+    r = D.upload(np.random.default_rng(22).standard_normal(M.nrows))
+    z_host, z_dev = D.empty(M.nrows), D.empty(M.nrows)
+    dev.hostcycle(r, z_host, "k")
+    dev.cycle(r, z_dev, "k")
+    np.testing.assert_allclose(z_dev.cpu().numpy(), z_host.cpu().numpy(), rtol=1e-9, atol=1e-12)
+
+
 def test_cpr_product_form_identity(gpu):
     """Eq. 8 (tests/test_cpr.py:98-118): I - B A = (I - R A)(I - Pi B_P Pi^T A)."""
     rng = np.random.default_rng(20240817)
