@@ -261,6 +261,10 @@ int cprb_prolong(const cprb_amg_level* lvl, const double* xc, double* x, void* s
 int cprb_kcycle_create(const cprb_amg* h, const cprb_sell* level_spmv, int32_t pre_sweeps,
                        int32_t post_sweeps, void** plan);
 int cprb_kcycle_destroy(void* plan);
+/* K-cycle coarse correction from level l >= 1 (src/amg.py:256-263) on
+ * natural-order vectors (perm: level-permuted row -> natural index). */
+int cprb_kcycle_correction(const cprb_amg* h, int32_t l, const int32_t* perm, const double* rhs,
+                           double* out, void* stream);
 
 /* src/ilu.py:196-223  z = U^{-1} L^{-1} r (level-ordered, sync-free). */
 int cprb_bilu_apply(const cprb_bilu* F, const double* r, double* z, double* work_l,

@@ -98,6 +98,7 @@ _SIGS = {
     "cprb_pack_bsr_sell": (C.c_int, [C.c_int64, C.c_int32, vp, vp, vp, vp, vp, vp, vp]),
     "cprb_kcycle_create": (C.c_int, [vp, vp, C.c_int32, C.c_int32, vp]),
     "cprb_kcycle_destroy": (C.c_int, [vp]),
+    "cprb_kcycle_correction": (C.c_int, [vp, C.c_int32, vp, vp, vp, vp]),
     "cprb_wave_solve_part": (C.c_int, [vp, C.c_int32, C.c_int32, C.c_int32, vp, vp, vp, vp, vp]),
     "cprb_l_to_u_rows": (C.c_int, [vp, C.c_int32, C.c_int32, vp, vp, vp]),
     "cprb_wave_combine_rows": (C.c_int, [vp, C.c_int32, C.c_int32, vp, vp, vp, vp]),

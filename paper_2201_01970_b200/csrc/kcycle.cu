@@ -386,6 +386,34 @@ int cprb_kcycle_create(const cprb_amg* h, const cprb_sell* level_spmv, int32_t p
   return check_launch("kcycle create");
 }
 
+// K-cycle coarse correction from level l (src/amg.py:256-263): two Krylov
+// steps at level l preconditioned by the cycle at l, or the coarse solve when
+// l is the coarsest level.  rhs / out are in the level's natural order
+// (perm: level-permuted row -> natural index).  Used by the slab-partitioned
+// solve, whose level 0 is distributed while levels >= 1 live on rank 0.
+int cprb_kcycle_correction(const cprb_amg* h, int32_t l, const int32_t* perm, const double* rhs,
+                           double* out, void* stream) {
+  const KPlan* P = static_cast<const KPlan*>(h->kwork);
+  if (!P) return set_error(CPRB_EINVAL, "K-cycle plan missing (cprb_kcycle_create)");
+  if (l < 1 || l >= h->nlevels) return set_error(CPRB_EINVAL, "level out of range");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n = P->n[l];
+  double* bl = P->rc[l - 1];  // level-l right-hand side buffer (permuted order)
+  k_kgather<<<kfull(n), 256, 0, st>>>(n, perm, rhs, 1, bl);
+  const double* xl;
+  if (l == h->nlevels - 1) {
+    k_kdense<<<kfull((int64_t)h->n_coarse * 32), 256, 0, st>>>(h->n_coarse, h->coarse_inv, bl,
+                                                              P->coarse_x);
+    xl = P->coarse_x;
+  } else {
+    const int rc = h->use_fcg ? fcg_at(*P, *h, l, bl, st) : fgmres_at(*P, *h, l, bl, st);
+    if (rc) return rc;
+    xl = P->x[l];
+  }
+  k_kscatter<<<kfull(n), 256, 0, st>>>(n, perm, xl, out);
+  return check_launch("kcycle correction");
+}
+
 int cprb_kcycle_destroy(void* plan) {
   delete static_cast<KPlan*>(plan);
   return CPRB_OK;

@@ -612,8 +612,7 @@ class SlabCpr:
         one rank, replicated otherwise (ranks sharing a GPU: tests)."""
         D.require_cuda()
         h = B.pressure_solver
-        if h.params.cycle != "v":
-            raise NotImplementedError("the slab-partitioned path runs the V-cycle")
+        self.cycle = h.params.cycle
         if len(h.levels) < 2:
             raise NotImplementedError("the slab-partitioned path needs at least two AMG levels")
         self.part, self.comm = part, comm
@@ -628,9 +627,18 @@ class SlabCpr:
         self.b1 = D.zeros(self.n1)
         self.e1 = D.zeros(self.n1)
         self.sub = None
+        self.kfull = None
         if rank == 0:
-            sub = AmgHierarchy(h.levels[1:], h.coarsest_lu, h.params, symmetric=h.symmetric)
-            self.sub = DeviceAmg(sub, 1)
+            if self.cycle == "k":
+                # K: the coarse correction of level 0 is the Krylov-wrapped
+                # recursion from level 1 (src/amg.py:256-263), on rank 0
+                self.kfull = DeviceAmg(h, 1)
+                if self.kfull.kdesc() is None:
+                    raise NotImplementedError("slab-partitioned K-cycle needs the device K-cycle")
+                self.perm1 = D.upload(self.kfull.perms[1].astype(np.int32))
+            else:
+                sub = AmgHierarchy(h.levels[1:], h.coarsest_lu, h.params, symmetric=h.symmetric)
+                self.sub = DeviceAmg(sub, 1)
         if bilu == "auto":
             bilu = "wave" if (comm.nccl or comm.size == 1) else "replicated"
         self.bilu_mode = bilu
@@ -664,6 +672,9 @@ class SlabCpr:
         self.gather1(comm, L0.bc, L0.n_agg, self.b1, root_only=True)
         if self.sub is not None:
             N.check(lib.cprb_amg_cycle(C.byref(self.sub.desc), D.ptr(self.b1), D.ptr(self.e1), st))
+        elif self.kfull is not None:
+            N.check(lib.cprb_kcycle_correction(C.byref(self.kfull.kdesc()), 1, D.ptr(self.perm1),
+                                               D.ptr(self.b1), D.ptr(self.e1), st))
         comm.broadcast(self.e1, 0)
         N.check(lib.cprb_prolong(d, D.ptr(self.e1), D.ptr(L0.x), st))
         L0.exchange_x(comm)
