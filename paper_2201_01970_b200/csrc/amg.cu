@@ -981,19 +981,24 @@ extern "C" int cprb_pgs_scm_color(const cprb_amg_level* lvl, int32_t k, double* 
   const cprb_amg_level& L = *lvl;
   cudaStream_t st = (cudaStream_t)stream;
   if (k < 0 || k >= L.ncolors) return set_error(CPRB_EINVAL, "colour index out of range");
-  if (L.color_snapshot && L.color_snapshot[k])
-    return set_error(CPRB_EUNSUPPORTED, "snapshot colours are not supported per colour");
+  // a colour with intra-colour couplings reads the snapshot of x taken at
+  // the colour's start (src/smoothers.py:301-308): write to tmp, copy back
+  const bool snap = L.color_snapshot && L.color_snapshot[k];
+  double* xo = snap ? L.tmp : x;
   const int code = (zero_guess ? 4 : 0) + (gsrc ? 2 : 0) + (sout ? 1 : 0);
   switch (code) {
-    case 0: launch_sweep<0, 0, 0>(L, k, b, gsrc, gstride, perm, x, x, sout, st); break;
-    case 1: launch_sweep<0, 0, 1>(L, k, b, gsrc, gstride, perm, x, x, sout, st); break;
-    case 2: launch_sweep<0, 1, 0>(L, k, b, gsrc, gstride, perm, x, x, sout, st); break;
-    case 3: launch_sweep<0, 1, 1>(L, k, b, gsrc, gstride, perm, x, x, sout, st); break;
-    case 4: launch_sweep<1, 0, 0>(L, k, b, gsrc, gstride, perm, x, x, sout, st); break;
-    case 5: launch_sweep<1, 0, 1>(L, k, b, gsrc, gstride, perm, x, x, sout, st); break;
-    case 6: launch_sweep<1, 1, 0>(L, k, b, gsrc, gstride, perm, x, x, sout, st); break;
-    default: launch_sweep<1, 1, 1>(L, k, b, gsrc, gstride, perm, x, x, sout, st); break;
+    case 0: launch_sweep<0, 0, 0>(L, k, b, gsrc, gstride, perm, x, xo, sout, st); break;
+    case 1: launch_sweep<0, 0, 1>(L, k, b, gsrc, gstride, perm, x, xo, sout, st); break;
+    case 2: launch_sweep<0, 1, 0>(L, k, b, gsrc, gstride, perm, x, xo, sout, st); break;
+    case 3: launch_sweep<0, 1, 1>(L, k, b, gsrc, gstride, perm, x, xo, sout, st); break;
+    case 4: launch_sweep<1, 0, 0>(L, k, b, gsrc, gstride, perm, x, xo, sout, st); break;
+    case 5: launch_sweep<1, 0, 1>(L, k, b, gsrc, gstride, perm, x, xo, sout, st); break;
+    case 6: launch_sweep<1, 1, 0>(L, k, b, gsrc, gstride, perm, x, xo, sout, st); break;
+    default: launch_sweep<1, 1, 1>(L, k, b, gsrc, gstride, perm, x, xo, sout, st); break;
   }
+  const int s0 = L.color_slices[k], s1 = L.color_slices[k + 1];
+  if (snap && s1 > s0)
+    k_copy_rows<<<nblk((int64_t)(s1 - s0) * 32, 256), 256, 0, st>>>(L.smoother, s0, s1, L.tmp, x);
   return check_launch("pgs colour");
 }
 

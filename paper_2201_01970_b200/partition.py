@@ -322,9 +322,14 @@ class SlabLevel0:
         ent_gp = sp.off_cols[src]
         ent_v = sp.off_vals[src]
         rk = kcol[row_of]
-        if np.any((ent_gp >= crg[rk]) & (ent_gp < crg[rk + 1])):
-            raise NotImplementedError("slab partition: level 0 has intra-colour couplings "
-                                      "(snapshot colours, theta_amg > 0)")
+        # colours with intra-colour couplings sweep against a snapshot
+        # (src/smoothers.py:301-308); a GLOBAL property of the colour
+        g_rows = np.repeat(np.arange(sp.n, dtype=np.int64), np.diff(sp.off_ptr))
+        g_k = np.searchsorted(crg, g_rows, side="right") - 1
+        intra = (sp.off_cols >= crg[g_k]) & (sp.off_cols < crg[g_k + 1])
+        snap = np.zeros(max(ncol, 1), dtype=np.uint8)
+        if intra.any():
+            snap[np.unique(g_k[intra])] = 1
         ent_l = lidx(perm[ent_gp])
         lo_cnt = np.zeros(n_own, dtype=np.int64)
         np.add.at(lo_cnt, row_of[ent_gp < crg[rk]], 1)
@@ -348,7 +353,7 @@ class SlabLevel0:
         self.perm_local = D.upload((cells - c0).astype(np.int32))
         self.color_slices = np.asarray(slices, dtype=np.int32)
         self.color_rows = cr.astype(np.int32)
-        self.snapshot = np.zeros(max(ncol, 1), dtype=np.uint8)
+        self.snapshot = snap
         cw = np.zeros(2 * max(ncol, 1), dtype=np.int32)
         for k in range(ncol):
             a, e = int(slices[k]) * 32, int(slices[k + 1]) * 32

@@ -142,10 +142,10 @@ def _c1():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("cycle", ["v", "k"])
-def test_slab_n1_matches_single_gpu_and_reference(gpu, cycle):
+@pytest.mark.parametrize("cycle,theta", [("v", 0.0), ("k", 0.0), ("v", 0.08)])
+def test_slab_n1_matches_single_gpu_and_reference(gpu, cycle, theta):
     A, b = _c1()
-    cfg = P.SolverConfig(theta=0.0, theta_amg=0.0, cycle=cycle)
+    cfg = P.SolverConfig(theta=0.0, theta_amg=theta, cycle=cycle)
     outer, inner, conv, rel, hist, x = _slab_solve(A, b, cfg, 1, 0, 64)
     B = P.build_cpr(A, cfg)
     ref = P.gmres_solve(A, b, None, B, cfg.gmres_params(), history=True)
@@ -154,12 +154,12 @@ def test_slab_n1_matches_single_gpu_and_reference(gpu, cycle):
     # different (fixed) reduction trees: rounding-level differences only
     np.testing.assert_allclose(hist, h1, rtol=1e-9)
     assert np.linalg.norm(x - ref.x) <= 1e-11 * np.linalg.norm(ref.x)
-    g = load_golden(f"c1_{cycle}0.npz")                  # the unmodified reference's run
+    g = load_golden(f"c1_{cycle}{'0' if theta == 0.0 else 'd'}.npz")   # the reference's run
     np.testing.assert_allclose(hist, g["hist"], rtol=1e-8)
     assert np.linalg.norm(x - g["x"]) <= 1e-9 * np.linalg.norm(g["x"])
 
 
-def _slab_worker(rank, world, port, seg, shape, q, bilu="auto", cycle="v"):
+def _slab_worker(rank, world, port, seg, shape, q, bilu="auto", cycle="v", theta=0.0):
     sys.path.insert(0, str(ROOT))
     sys.path.insert(0, str(ROOT / "tests"))
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -167,7 +167,7 @@ def _slab_worker(rank, world, port, seg, shape, q, bilu="auto", cycle="v"):
         torch.cuda.set_device(0)                          # every rank shares the one GPU
         dist.init_process_group("gloo", rank=rank, world_size=world)
         A, b = _grid(*shape)
-        cfg = P.SolverConfig(theta=0.0, theta_amg=0.0, cycle=cycle)
+        cfg = P.SolverConfig(theta=0.0, theta_amg=theta, cycle=cycle)
         out = _slab_solve(A, b, cfg, world, rank, seg, bilu=bilu)
         q.put((rank, out))
         dist.destroy_process_group()
@@ -177,16 +177,18 @@ def _slab_worker(rank, world, port, seg, shape, q, bilu="auto", cycle="v"):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,cycle", [(2, "v"), (3, "v"), (2, "k")])
-def test_slab_ranks_bitwise_equal_to_one_rank(gpu, world, cycle):
+@pytest.mark.parametrize("world,cycle,theta", [(2, "v", 0.0), (3, "v", 0.0), (2, "k", 0.0),
+                                               (2, "v", 0.08)])
+def test_slab_ranks_bitwise_equal_to_one_rank(gpu, world, cycle, theta):
     shape, seg = (12, 10, 14), 60
     A, b = _grid(*shape)
-    cfg = P.SolverConfig(theta=0.0, theta_amg=0.0, cycle=cycle)
+    cfg = P.SolverConfig(theta=0.0, theta_amg=theta, cycle=cycle)
     one = _slab_solve(A, b, cfg, 1, 0, seg, bilu="replicated")
     port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_slab_worker, args=(r, world, port, seg, shape, q, "auto", cycle))
+    procs = [ctx.Process(target=_slab_worker,
+                         args=(r, world, port, seg, shape, q, "auto", cycle, theta))
              for r in range(world)]
     for p in procs:
         p.start()
