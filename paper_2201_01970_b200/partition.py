@@ -286,6 +286,9 @@ class SlabLevel0:
         perm, inv = sp.perm, sp.inv
         crg = np.asarray(sp.color_rows, dtype=np.int64)
         ncol = sp.ncolors
+        if ncol < 2:
+            raise NotImplementedError("slab partition: a single-colour level 0 is a sequential "
+                                      "Gauss-Seidel sweep (src/smoothers.py:296-299)")
         gp = np.sort(inv[c0:c1])                        # global permuted positions
         cells = perm[gp]                                 # natural cell of each local row
         kcol = np.searchsorted(crg, gp, side="right") - 1
