@@ -80,6 +80,26 @@ def test_halo_plans_pair_up(N):
         assert win[1][0] == part.rows(1)[0] - 100
 
 
+def test_halo_plans_random_pattern():
+    """Unstructured pattern: windows span several ranks, every rank exchanges
+    with every other; sends and receives still pair up and cover the halo."""
+    from conftest import random_block
+    rng = np.random.default_rng(3)
+    Ao = random_block(rng, 400, 3)
+    A = P.BlockCsrMatrix(3, Ao.nrows, Ao.ncols, Ao.ptr, Ao.cols, Ao.vals)
+    for N in (2, 3, 5):
+        part = SlabPartition(A.nrows, N, 16)
+        win = _windows(A, part)
+        plans = [halo_plan(part, win, p) for p in range(N)]
+        for p in range(N):
+            a, e = part.rows(p)
+            for q in range(N):
+                assert ([(x, y) for r, x, y in plans[p][0] if r == q]
+                        == [(x, y) for r, x, y in plans[q][1] if r == p])
+            got = sorted(c for _, x, y in plans[p][1] for c in range(x, y))
+            assert got == [c for c in range(win[p][0], win[p][1]) if not a <= c < e]
+
+
 def _comm_worker(rank, world, port, q):
     sys.path.insert(0, str(ROOT))
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -339,3 +359,54 @@ def test_wave_plan_cuts(N):
             want = np.unique(slot[np.unique(cols[cross & (owner[rows] == q)])])
             assert np.array_equal(np.sort(h["mirror"][q]), want)
         assert cross.any()
+
+
+def _random_worker(rank, world, port, q):
+    sys.path.insert(0, str(ROOT))
+    sys.path.insert(0, str(ROOT / "tests"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    try:
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        q.put((rank, _random_solve(world, rank)))
+        dist.destroy_process_group()
+    except Exception as exc:  # pragma: no cover
+        import traceback
+        q.put((rank, ("error", repr(exc), traceback.format_exc())))
+
+
+def _random_solve(N, rank):
+    from conftest import random_block
+    from paper_2201_01970_b200.partition import gather_rows, gmres_solve_slab
+    rng = np.random.default_rng(5)
+    Ao = random_block(rng, 300, 3)
+    A = P.BlockCsrMatrix(3, Ao.nrows, Ao.ncols, Ao.ptr, Ao.cols, Ao.vals)
+    b = rng.standard_normal(900)
+    part = SlabPartition(A.nrows, N, 16)
+    comm = SlabComm()
+    a, e = part.rows(rank)
+    res = gmres_solve_slab(A, torch.from_numpy(b[3 * a:3 * e].copy()).cuda(), None, None,
+                           P.GmresParams(m=30, tol=1e-10, max_restarts=20), comm=comm, part=part,
+                           history=True)
+    x = gather_rows(res.x, part, comm, 3).cpu().numpy()
+    return res.outer, res.inner, [h if not isinstance(h, tuple) else -h[1] for h in res.history], x
+
+
+@pytest.mark.gpu
+def test_slab_unstructured_all_to_all_halo(gpu):
+    """Unpreconditioned partitioned GMRES on an unstructured block matrix:
+    every rank's window spans the others (multi-peer halo exchange); 3 ranks
+    bitwise equal to 1."""
+    one = _random_solve(1, 0)
+    world, port = 3, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_random_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+    for r in range(world):
+        assert got[r][0] != "error", got[r]
+        assert got[r][:3] == one[:3] and np.array_equal(got[r][3], one[3])
