@@ -237,6 +237,8 @@ def run_ours(args):
         _ = r2.x.numpy()
         te.append(time.perf_counter() - t0)
     e2e_ms = float(np.median(te) * 1e3)
+    if ws > 1:
+        e2e_ms = max_over_ranks(e2e_ms, dist, torch, "cuda")
     small = sum((j + 2) * 8 + 16 for j in range(res.inner)) + 8 * (3 + 2 * res.outer)
 
     # per-kernel timing on the launching stream (CUDA events), algorithmic bytes
