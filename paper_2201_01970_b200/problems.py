@@ -170,6 +170,30 @@ def _assemble(g: _Grid, perm, conv_scale, couple, drift) -> BlockCsrMatrix:
     return BlockCsrMatrix(3, n, n, g.ptr, g.cols, vals)
 
 
+def _rhs(A: BlockCsrMatrix, xs: np.ndarray) -> np.ndarray:
+    """b = A x* for input generation: on the B200 when one is present (the
+    bit-exact device SpMV; the matrix stays resident for the solve that
+    follows), else on the host in the same order."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            from . import device as D
+            return _rhs_device(A, xs)
+    except (ImportError, OSError, RuntimeError):
+        pass
+    return bsr_matvec_reference_order(A, xs)
+
+
+def _rhs_device(A: BlockCsrMatrix, xs: np.ndarray) -> np.ndarray:
+    from . import _native as N
+    from . import device as D
+    M = D.device_matrix(A)
+    x = D.upload(np.ascontiguousarray(xs, dtype=np.float64))
+    y = D.empty(A.nrows * A.block_size)
+    N.check(N.lib().cprb_spmv(M.desc_ref(), A.block_size, D.ptr(x), D.ptr(y), None, D.stream()))
+    return y.cpu().numpy()
+
+
 def generate_blackoil_like_sequence(nx: int, ny: int, nz: int, nsteps: int, drift: float,
                                     seed: int, with_rhs: bool = True) -> ProblemSequence:
     """Deterministic-by-seed sequence of 3x3-block 7-point systems
@@ -189,7 +213,7 @@ def generate_blackoil_like_sequence(nx: int, ny: int, nz: int, nsteps: int, drif
             logk = logk + drift * rng.normal(0.0, 1.0, n)
             conv_scale = conv_scale * np.exp(drift * rng.normal(0.0, 1.0, n))
         A = _assemble(g, np.exp(logk), conv_scale, couple, drift)
-        systems.append((A, bsr_matvec_reference_order(A, xs) if with_rhs else None))
+        systems.append((A, _rhs(A, xs) if with_rhs else None))
     return ProblemSequence(systems, provenance={"kind": "synthetic", "nx": nx, "ny": ny,
                                                 "nz": nz, "nsteps": nsteps, "drift": drift,
                                                 "seed": seed})

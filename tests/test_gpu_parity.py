@@ -76,6 +76,14 @@ def test_spmv_c1_rhs_and_long_rows(gpu):
     del gen
 
 
+def test_generator_rhs_device_equals_host_order(gpu):
+    """Input generation computes b = A x* with the device SpMV when a GPU is
+    present: bitwise equal to the host reference-order product."""
+    (A, b), = P.generate_blackoil_like_sequence(23, 17, 9, 1, 0.01, 5).systems
+    xs = P.problems.manufactured_solution(A.nrows)
+    assert np.array_equal(b, P.problems.bsr_matvec_reference_order(A, xs))
+
+
 def test_device_sell_packing_matches_host_layout(gpu, rng):
     """Jacobian uploads pack SELL-32 on the device (csrc/spmv.cu
     k_pack_bsr_sell): identical arrays to the host packer."""
