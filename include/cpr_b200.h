@@ -194,6 +194,8 @@ typedef struct cprb_wave {
   const int64_t* rhs_off;      /* dev, double offsets into the rhs vector */
   const int32_t* rhs_bytes;    /* dev */
   const uint8_t* stream;       /* dev */
+  int32_t max_chunk_steps;     /* longest chunk (steps); <= 320: metadata staged in smem */
+  int32_t pad_;
 } cprb_wave;
 
 typedef struct cprb_bilu {

@@ -60,7 +60,7 @@ class Wave(C.Structure):
     _fields_ = [("nchunks", C.c_int32), ("nsteps", C.c_int32), ("stage_max", C.c_int32),
                 ("rhs_max", C.c_int32), ("chunk_step", vp), ("step_off", vp), ("step_bytes", vp),
                 ("step_w", vp), ("step_k", vp), ("rhs_off", vp), ("rhs_bytes", vp),
-                ("stream", vp)]
+                ("stream", vp), ("max_chunk_steps", C.c_int32), ("pad_", C.c_int32)]
 
 
 class Bilu(C.Structure):

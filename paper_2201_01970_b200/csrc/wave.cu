@@ -264,7 +264,7 @@ __device__ __noinline__ void row_general(const uint8_t* blk, int K, const double
 // UPPER = false: z = r - sum L z         (z published in L-step order)
 // UPPER = true : y = Uinv (z - sum U y)   (y published in U-step order)
 // out_step must hold the sentinel (armed by the caller) wherever it is polled.
-template <int B, bool UPPER>
+template <int B, bool UPPER, bool STG>
 __global__ void __launch_bounds__(WAVE_THREADS, 1)
     k_wave(const cprb_wave W, const double* __restrict__ rhs_steps, double* out_step,
            int32_t* ticket, double* peer_out) {
@@ -303,7 +303,9 @@ __global__ void __launch_bounds__(WAVE_THREADS, 1)
     if (c >= W.nchunks) break;
     const int s0 = W.chunk_step[c];
     const int s1 = W.chunk_step[c + 1];
-    const bool staged = (s1 - s0) <= WAVE_META;
+    // STG: every chunk's step metadata fits in shared memory (checked by the
+    // host), so the per-step global fallback is compiled out
+    const bool staged = STG || (s1 - s0) <= WAVE_META;
     if (staged) {
       for (int k = s0 + tid; k < s1; k += blockDim.x) {
         StepMeta m;
@@ -319,7 +321,7 @@ __global__ void __launch_bounds__(WAVE_THREADS, 1)
     if (tid < WAVE_NWARPS) s_prog[tid] = s0 - 1;
     __syncthreads();
     auto meta = [&](int k) -> StepMeta {
-      if (staged) return s_meta[k - s0];
+      if (STG || staged) return s_meta[k - s0];
       StepMeta m;
       m.off = W.step_off[k];
       m.rhs_off = W.rhs_off[k];
@@ -461,10 +463,14 @@ static int launch_wave(const cprb_wave& W, const double* rhs_steps, double* out_
   // running work; concurrent slab solves on other streams must not wait)
   static size_t smem_set = 0;
   if (smem > smem_set) {
-    cudaFuncSetAttribute(k_wave<B, UPPER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_wave<B, UPPER, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_wave<B, UPPER, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     smem_set = smem;
   }
-  k_wave<B, UPPER><<<grid, WAVE_THREADS, smem, st>>>(W, rhs_steps, out_step, ticket, peer_out);
+  if (W.max_chunk_steps > 0 && W.max_chunk_steps <= WAVE_META)
+    k_wave<B, UPPER, true><<<grid, WAVE_THREADS, smem, st>>>(W, rhs_steps, out_step, ticket, peer_out);
+  else
+    k_wave<B, UPPER, false><<<grid, WAVE_THREADS, smem, st>>>(W, rhs_steps, out_step, ticket, peer_out);
   return check_launch("wave solve");
 }
 

@@ -318,10 +318,12 @@ class WaveDev:
         self.host = host
         self.t = {k: D.upload(host[k]) for k in ("chunk_step", "step_off", "step_bytes", "step_w",
                                                  "step_k", "rhs_off", "rhs_bytes", "stream")}
+        cs = np.asarray(host["chunk_step"], dtype=np.int64)
+        mcs = int(np.diff(cs).max()) if cs.shape[0] > 1 else 0
         self.desc = N.Wave(host["nchunks"], host["nsteps"], host["stage_max"], host["rhs_max"],
                            *[D.ptr(self.t[k]) for k in ("chunk_step", "step_off", "step_bytes",
                                                          "step_w", "step_k", "rhs_off",
-                                                         "rhs_bytes", "stream")])
+                                                         "rhs_bytes", "stream")], mcs, 0)
 
 
 class DeviceBilu:
