@@ -161,7 +161,10 @@ __device__ __forceinline__ void ring_value(const Ring& ring, int k, int q, doubl
 template <int B, bool UPPER, int K>
 __device__ __forceinline__ void row_fast(uint32_t sblk, uint32_t srhs, int l, int len,
                                          const Ring& ring, int k, const double* glob,
-                                         double* res) {
+                                         double* res, int kr) {
+  // K: register extent (the largest dependency count served); kr: the
+  // step's record layout (its K); rows with len < K are predicated, and the
+  // reduceat order of segsum_masked depends on len only
   constexpr int BB = B * B;
   constexpr int KA = K > 0 ? K : 1;
   int code[KA];
@@ -171,7 +174,7 @@ __device__ __forceinline__ void row_fast(uint32_t sblk, uint32_t srhs, int l, in
     code[m] = (m < len) ? lds_s32(sblk + 4u * (96 + 32 * m + l)) : 0;
 #pragma unroll
     for (int e = 0; e < BB; ++e)
-      mv[m][e] = (m < len) ? lds_f64(sblk + 4u * (96 + 32 * K) + 8u * ((m * BB + e) * 32 + l)) : 0.0;
+      mv[m][e] = (m < len) ? lds_f64(sblk + 4u * (96 + 32 * kr) + 8u * ((m * BB + e) * 32 + l)) : 0.0;
   }
   double rh[B];
 #pragma unroll
@@ -207,7 +210,7 @@ __device__ __forceinline__ void row_fast(uint32_t sblk, uint32_t srhs, int l, in
     }
   }
   if constexpr (UPPER) {
-    const uint32_t a_ui = sblk + 4u * (96 + 32 * K) + 8u * (K * BB * 32);
+    const uint32_t a_ui = sblk + 4u * (96 + 32 * kr) + 8u * (kr * BB * 32);
     double ui[BB];
 #pragma unroll
     for (int e = 0; e < BB; ++e) ui[e] = lds_f64(a_ui + 8u * (e * 32 + l));
@@ -386,12 +389,8 @@ __global__ void __launch_bounds__(WAVE_THREADS, 1)
           const int len = lenw & WAVE_LEN_MASK;
           double res[B];
           if (fast) {
-            switch (mk.k) {
-              case 0: row_fast<B, UPPER, 0>(sblk, srhs, lane, len, ring, k, out_step, res); break;
-              case 1: row_fast<B, UPPER, 1>(sblk, srhs, lane, len, ring, k, out_step, res); break;
-              case 2: row_fast<B, UPPER, 2>(sblk, srhs, lane, len, ring, k, out_step, res); break;
-              default: row_fast<B, UPPER, 3>(sblk, srhs, lane, len, ring, k, out_step, res); break;
-            }
+            // one instantiation for every streamed step (smaller hot loop)
+            row_fast<B, UPPER, WAVE_KMAX>(sblk, srhs, lane, len, ring, k, out_step, res, mk.k);
           } else {
             row_general<B, UPPER>(gblk, mk.k, grhs, lane, len, ring, k, out_step, res);
           }
