@@ -144,7 +144,7 @@ struct Ring {
 
 // value of an in-chunk dependency (code q = (diff-1) * THREADS + position)
 template <int B>
-__device__ __forceinline__ void ring_value(const Ring& ring, int k, int q, double* v) {
+__device__ __forceinline__ void ring_value(const Ring ring, int k, int q, double* v) {
   const int diff = q / WAVE_THREADS + 1;
   const int pos = q - (diff - 1) * WAVE_THREADS;
   const int dstep = k - diff;
@@ -160,7 +160,7 @@ __device__ __forceinline__ void ring_value(const Ring& ring, int k, int q, doubl
 // `base` is a shared (space = 1) or generic (space = 0) address.
 template <int B, bool UPPER, int K>
 __device__ __forceinline__ void row_fast(uint32_t sblk, uint32_t srhs, int l, int len,
-                                         const Ring& ring, int k, const double* glob,
+                                         const Ring ring, int k, const double* glob,
                                          double* res, int kr) {
   // K: register extent (the largest dependency count served); kr: the
   // step's record layout (its K); rows with len < K are predicated, and the
@@ -226,7 +226,7 @@ __device__ __forceinline__ void row_fast(uint32_t sblk, uint32_t srhs, int l, in
 // reads the warp slice straight from global memory
 template <int B, bool UPPER>
 __device__ __noinline__ void row_general(const uint8_t* blk, int K, const double* rhs, int l,
-                                         int len, const Ring& ring, int k, const double* glob,
+                                         int len, const Ring ring, int k, const double* glob,
                                          double* res) {
   constexpr int BB = B * B;
   const int32_t* codes = reinterpret_cast<const int32_t*>(blk) + 96;
