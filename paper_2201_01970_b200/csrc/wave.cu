@@ -392,7 +392,12 @@ __global__ void __launch_bounds__(WAVE_THREADS, 1)
             // one instantiation for every streamed step (smaller hot loop)
             row_fast<B, UPPER, WAVE_KMAX>(sblk, srhs, lane, len, ring, k, out_step, res, mk.k);
           } else {
-            row_general<B, UPPER>(gblk, mk.k, grhs, lane, len, ring, k, out_step, res);
+            // the out-of-line path gets its own buffer so that res itself
+            // never needs an address (stays in registers on the fast path)
+            double rg[B];
+            row_general<B, UPPER>(gblk, mk.k, grhs, lane, len, ring, k, out_step, rg);
+#pragma unroll
+            for (int r = 0; r < B; ++r) res[r] = rg[r];
           }
           const uint32_t slot = (uint32_t)((k % WAVE_RING) * WAVE_THREADS + pos);
 #pragma unroll
