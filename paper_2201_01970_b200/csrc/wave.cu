@@ -56,6 +56,8 @@ __device__ __forceinline__ void st_relaxed_sys(double* p, double v) {
 // %globaltimer when row position 0 of the step finished; nullptr = off
 __device__ unsigned long long* g_wave_log = nullptr;
 
+static bool g_wave_log_on = false;  // host mirror of g_wave_log != nullptr
+
 constexpr int WAVE_LOG_STEPS = 512;
 constexpr int WAVE_LOG_CHUNKS = 256;
 
@@ -267,12 +269,13 @@ __device__ __noinline__ void row_general(const uint8_t* blk, int K, const double
 // UPPER = false: z = r - sum L z         (z published in L-step order)
 // UPPER = true : y = Uinv (z - sum U y)   (y published in U-step order)
 // out_step must hold the sentinel (armed by the caller) wherever it is polled.
-template <int B, bool UPPER, bool STG>
+template <int B, bool UPPER, bool STG, bool TL>
 __global__ void __launch_bounds__(WAVE_THREADS, 1)
     k_wave(const cprb_wave W, const double* __restrict__ rhs_steps, double* out_step,
            int32_t* ticket, double* peer_out) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  unsigned long long* const tlog = g_wave_log;  // diagnostic timeline (read once)
+  // diagnostic timeline, compiled in only for the TL variant
+  unsigned long long* const tlog = TL ? g_wave_log : nullptr;
   __shared__ StepMeta s_meta[WAVE_META];
   __shared__ __align__(8) uint64_t s_full[WAVE_NWARPS][WAVE_DEPTH];
   __shared__ int s_prog[WAVE_NWARPS];
@@ -416,7 +419,7 @@ __global__ void __launch_bounds__(WAVE_THREADS, 1)
               for (int r = 0; r < B; ++r) st_relaxed_sys(q + r, res[r]);
             }
           }
-          if (pos == 0 && tlog && c < WAVE_LOG_CHUNKS && k - s0 < WAVE_LOG_STEPS) {
+          if (TL && pos == 0 && tlog && c < WAVE_LOG_CHUNKS && k - s0 < WAVE_LOG_STEPS) {
             unsigned long long tt;
             asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tt));
             tlog[((UPPER ? 1 : 0) * WAVE_LOG_CHUNKS + c) * WAVE_LOG_STEPS + (k - s0)] = tt;
@@ -467,14 +470,20 @@ static int launch_wave(const cprb_wave& W, const double* rhs_steps, double* out_
   // running work; concurrent slab solves on other streams must not wait)
   static size_t smem_set = 0;
   if (smem > smem_set) {
-    cudaFuncSetAttribute(k_wave<B, UPPER, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_wave<B, UPPER, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_wave<B, UPPER, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_wave<B, UPPER, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_wave<B, UPPER, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_wave<B, UPPER, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     smem_set = smem;
   }
-  if (W.max_chunk_steps > 0 && W.max_chunk_steps <= WAVE_META)
-    k_wave<B, UPPER, true><<<grid, WAVE_THREADS, smem, st>>>(W, rhs_steps, out_step, ticket, peer_out);
-  else
-    k_wave<B, UPPER, false><<<grid, WAVE_THREADS, smem, st>>>(W, rhs_steps, out_step, ticket, peer_out);
+  const bool stg = W.max_chunk_steps > 0 && W.max_chunk_steps <= WAVE_META;
+  if (g_wave_log_on) {
+    if (stg) k_wave<B, UPPER, true, true><<<grid, WAVE_THREADS, smem, st>>>(W, rhs_steps, out_step, ticket, peer_out);
+    else k_wave<B, UPPER, false, true><<<grid, WAVE_THREADS, smem, st>>>(W, rhs_steps, out_step, ticket, peer_out);
+  } else {
+    if (stg) k_wave<B, UPPER, true, false><<<grid, WAVE_THREADS, smem, st>>>(W, rhs_steps, out_step, ticket, peer_out);
+    else k_wave<B, UPPER, false, false><<<grid, WAVE_THREADS, smem, st>>>(W, rhs_steps, out_step, ticket, peer_out);
+  }
   return check_launch("wave solve");
 }
 
@@ -541,6 +550,7 @@ int wave_combine(const cprb_bilu& F, const double* zp, double* z, cudaStream_t s
 extern "C" int cprb_wave_set_log(uint64_t* dev_log) {
   unsigned long long* p = (unsigned long long*)dev_log;
   cudaMemcpyToSymbol(cprb::g_wave_log, &p, sizeof(p));
+  cprb::g_wave_log_on = p != nullptr;
 
   return cprb::check_launch("wave log");
 }
