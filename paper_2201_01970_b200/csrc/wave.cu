@@ -144,6 +144,20 @@ struct Ring {
   uint32_t flag;  // smem: RING * WAVE_THREADS ints (global step index held)
 };
 
+__device__ __forceinline__ int lds_relaxed_s32(uint32_t a) {
+  int v;
+  asm volatile("ld.relaxed.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+
+// ring slot of an in-chunk dependency (code q = (diff-1) * THREADS + position)
+__device__ __forceinline__ uint32_t ring_slot(int k, int q, int& dstep) {
+  const int diff = q / WAVE_THREADS + 1;
+  const int pos = q - (diff - 1) * WAVE_THREADS;
+  dstep = k - diff;
+  return (uint32_t)((dstep % WAVE_RING) * WAVE_THREADS + pos);
+}
+
 // value of an in-chunk dependency (code q = (diff-1) * THREADS + position)
 template <int B>
 __device__ __forceinline__ void ring_value(const Ring ring, int k, int q, double* v) {
@@ -189,11 +203,27 @@ __device__ __forceinline__ void row_fast(uint32_t sblk, uint32_t srhs, int l, in
     if (m < len && code[m] >= 0)
 #pragma unroll
       for (int c = 0; c < B; ++c) dv[m][c] = ld_relaxed(glob + (int64_t)code[m] + c);
+  // in-chunk dependencies: poll all flags with relaxed loads, then one
+  // acquire fence before reading the values (instead of one acquire each)
+  uint32_t rslot[KA];
+#pragma unroll
+  for (int m = 0; m < K; ++m)
+    if (m < len && code[m] < 0) {
+      int dstep;
+      rslot[m] = ring_slot(k, -code[m] - 1, dstep);
+      while (lds_relaxed_s32(ring.flag + 4u * rslot[m]) != dstep) {
+      }
+    }
+  asm volatile("fence.acq_rel.cta;" ::: "memory");
 #pragma unroll
   for (int m = 0; m < K; ++m) {
     if (m < len) {
-      if (code[m] < 0) ring_value<B>(ring, k, -code[m] - 1, dv[m]);
-      else wait_block<B>(glob + (int64_t)code[m], dv[m]);
+      if (code[m] < 0) {
+#pragma unroll
+        for (int c = 0; c < B; ++c) dv[m][c] = lds_f64(ring.vals + 8u * (rslot[m] * B + c));
+      } else {
+        wait_block<B>(glob + (int64_t)code[m], dv[m]);
+      }
     } else {
 #pragma unroll
       for (int c = 0; c < B; ++c) dv[m][c] = 0.0;
