@@ -17,9 +17,15 @@ identical on every rank because setup is deterministic) and uploads:
 * levels >= 1 are agglomerated on rank 0 (gather the level-1 right-hand
   side, run the device V-cycle from level 1, broadcast the correction), as
   the north star specifies;
-* BILU(0) (src/ilu.py:196-223) is a global wavefront that does not shard
-  (SURVEY.md 8(e)): the stage-2 residual is all-gathered and every rank runs
-  the full device solve, then keeps its rows.  It is the Amdahl term.
+* BILU(0) (src/ilu.py:196-223) is ONE global wavefront (SlabBilu): the wave
+  plans are cut at the slab boundaries, every rank runs its own chunks and
+  stores the rows its neighbour reads straight into the neighbour's output
+  array (CUDA IPC peer memory over NVLink), where they are polled like any
+  cross-chunk dependency.  The chain is sequential, so this is the Amdahl
+  term; bilu="replicated" (all-gather + full solve per rank) serves ranks
+  that share one GPU.
+* the K-cycle's coarse correction (Krylov steps from level 1) runs on rank 0
+  like the V-cycle's (cprb_kcycle_correction).
 
 Reductions are GPU-count invariant: fixed global segments, one partial per
 segment reduced in a fixed order by one CTA, all partials summed in global
