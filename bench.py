@@ -38,10 +38,16 @@ METRIC = "CPR-GMRES solve time & iters, SPE10-shape 3.28M DOF; smoother/SpMV HBM
 
 
 def _peaks():
+    """HBM roofline denominator: the driver-measured copy bandwidth when
+    MEASURED_PEAKS.json is present, else the profiling guide's fallback."""
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
-        d = json.loads(p.read_text())
-        return float(d.get("hbm_gbs", 6650.0)), "measured"
+        try:
+            v = float(json.loads(p.read_text())["hbm_gbs"])
+            if v > 0:
+                return v, "measured"
+        except (ValueError, KeyError, TypeError):
+            pass
     return 6650.0, "fallback"
 
 
