@@ -266,6 +266,32 @@ def make_small():
     (OUT / "summary.json").write_text(json.dumps(summary, indent=1) + "\n")
 
 
+def make_big_k():
+    """SPE10-shaped 60x220x85 (C3), theta_amg = 0, K-cycle (the reference's
+    default cycle, src/cpr.py:72): iteration counts, the Givens history of both
+    restarts and solution samples (about 12 minutes of CPU)."""
+    _import_ref()
+    from cprkit import cpr as cpr_mod
+    from cprkit.cpr import SolverConfig, build_cpr
+    from cprkit.problems import generate_blackoil_like_sequence
+    t0 = time.time()
+    seq = generate_blackoil_like_sequence(60, 220, 85, 1, 0.01, 0)
+    A, b = seq.systems[0]
+    tg = time.time() - t0
+    cfg = SolverConfig(theta=0.0, theta_amg=0.0, cycle="k")
+    t0 = time.time()
+    B = build_cpr(A, cfg)
+    ts = time.time() - t0
+    t0 = time.time()
+    res, hist = record_history(cpr_mod, A, b, B, cfg.gmres_params())
+    tsol = time.time() - t0
+    out = dict(outer=res.outer, inner=res.inner, rel=res.rel_residual, hist=hist.tolist(),
+               x_norm=float(np.linalg.norm(res.x)), x_sample_stride=97,
+               x_sample=res.x[::97].tolist(), b_digest=digest(b),
+               seconds=dict(generate=tg, setup=ts, solve=tsol))
+    (OUT / "c3_k0.json").write_text(json.dumps(out) + "\n")
+
+
 def make_big():
     """SPE10-shaped 60x220x85 (C3), theta_amg = 0, V-cycle: iteration counts,
     Givens history, solution samples, hierarchy digests."""
@@ -306,9 +332,12 @@ def make_big():
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
+    ap.add_argument("--bigk", action="store_true")
     ap.add_argument("--skip-small", action="store_true")
     a = ap.parse_args()
     if not a.skip_small:
         make_small()
     if a.big:
         make_big()
+    if a.bigk:
+        make_big_k()

@@ -486,16 +486,21 @@ def test_c2_pressure128_vcycle_against_survey(gpu):
 
 @pytest.mark.slow
 def test_c4_sequence_reuse_against_survey(gpu):
-    """Config 4 (first 3 of the 10 SPE10-shaped Newton systems, mu = 5, V,
-    theta_amg = 0): one setup, every solve 1 outer / 5 inner, final residuals
-    of the reference run within 1e-8 relative."""
-    seq = P.generate_blackoil_like_sequence(60, 220, 85, 3, 0.01, 0)
+    """Config 4 (all 10 SPE10-shaped Newton systems, mu = 5, V, theta_amg = 0):
+    one setup, every solve 1 outer / 5 inner, and the final residuals of the
+    reference run within 1e-8 relative -- the aging
+    reused preconditioner (stage 2 multiplies by the FIRST system's matrix,
+    src/cpr.py:185) must degrade exactly as the reference's does."""
+    seq = P.generate_blackoil_like_sequence(60, 220, 85, 10, 0.01, 0)
     cfg = P.SolverConfig(theta=0.0, theta_amg=0.0, cycle="v")
     out = P.ascpr_gmres_sequence(seq.systems, 5, cfg, keep_solutions=False)
     assert out.setup_calls == 1
-    assert [(r.outer, r.inner) for r in out.records] == [(1, 5)] * 3
-    assert [r.rebuilt for r in out.records] == [True, False, False]
-    ref = [4.539505890669102e-06, 4.81992118102329e-06, 5.0585008937417845e-06]
+    assert [(r.outer, r.inner) for r in out.records] == [(1, 5)] * 10
+    assert [r.rebuilt for r in out.records] == [True] + [False] * 9
+    ref = [4.539505890669102e-06, 4.81992118102329e-06, 5.0585008937417845e-06,
+           5.229715500921409e-06, 5.426977527133912e-06, 5.5681979247532605e-06,
+           5.6903747842288935e-06, 5.837020329973612e-06, 6.001836858286181e-06,
+           6.082489454699883e-06]
     np.testing.assert_allclose([r.rel_residual for r in out.records], ref, rtol=1e-8)
 
 

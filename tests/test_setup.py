@@ -201,3 +201,33 @@ def test_config_api():
         P.GmresParams(m=0)
     with pytest.raises(ValueError):
         P.AmgParams(cycle="w")
+
+
+@pytest.mark.slow
+def test_c3_setup_digests_against_reference():
+    """Config 3 (60x220x85): every structural digest the unmodified reference
+    recorded in tests/golden/c3_v0.json (make_golden.py --big): the Jacobian
+    values and rhs, and per pressure level the aggregates, the colour
+    permutation, the Galerkin values and columns, plus the BILU(0) level
+    counts.  Host setup only (reference: src/cpr.py:168-175,
+    src/amg.py:143-174, src/coloring.py:171-256, src/ilu.py:38-59)."""
+    ref = json.loads((GOLDEN / "c3_v0.json").read_text())
+    dg = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()  # noqa: E731
+    (A, b), = P.generate_blackoil_like_sequence(60, 220, 85, 1, 0.01, 0).systems
+    assert dg(A.values) == ref["vals_digest"]
+    assert dg(b) == ref["b_digest"]
+    B = P.build_cpr(A, P.SolverConfig(theta=0.0, theta_amg=0.0, cycle="v"))
+    h = B.pressure_solver
+    assert [l.A.nrows for l in h.levels] == ref["sizes"]
+    assert [l.A.nnz for l in h.levels] == ref["nnz"]
+    assert [l.partition.c if l.partition else None for l in h.levels] == ref["colors"]
+    for li, lvl in enumerate(h.levels):
+        assert dg(lvl.A.values) == ref["lvl_vals_digests"][li], li
+        assert dg(lvl.A.col_idx) == ref["lvl_cols_digests"][li], li
+        if lvl.aggregates is not None:
+            assert dg(lvl.aggregates) == ref["agg_digests"][li], li
+            assert dg(lvl.partition.perm()) == ref["perm_digests"][li], li
+        else:
+            assert ref["agg_digests"][li] is None
+    assert B.relaxation.l_schedule.n_levels == ref["bilu_llev"]
+    assert B.relaxation.u_schedule.n_levels == ref["bilu_ulev"]
