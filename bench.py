@@ -10,12 +10,14 @@ seed 0, drift 0.01) with SolverConfig(theta=0, theta_amg=0, cycle='v').
 `value` is the device time-to-solution in ms (inputs resident in HBM; the
 working set, > 1 GB, exceeds the 126 MB L2 so no flush is needed).  `e2e`
 is the same solve through the public API from pinned host buffers.
-`--impl reference` times the CPU oracle (oracle/cprkit_oracle.py, a numpy
-restatement of the reference) on the host cores.  For N > 1 every rank solves
-its own system (seed = rank; weak scaling, no data-path collective).
-`--partition` instead row-partitions ONE system over the N ranks (strong
-scaling; NCCL halo exchange and GPU-count-invariant reductions, DESIGN.md
-section 7).
+`--impl reference` times complete solves of the CPU oracle
+(oracle/cprkit_oracle.py, a numpy restatement of the reference) on the host
+cores, with the same config dict.  `--gpus N` (N > 1) relaunches itself as N
+torchrun ranks when WORLD_SIZE is unset; at N > 1 the default is ONE system
+row-partitioned over the N GPUs (strong scaling: NCCL halos, GPU-count-
+invariant reductions, the BILU wavefront over peer memory; DESIGN.md
+section 7) plus a config-5 (26.9M DOF) sub-record; `--replicas` solves N
+independent systems instead (weak scaling, no data-path collective).
 """
 
 from __future__ import annotations
@@ -140,6 +142,19 @@ def _config_name(grid) -> str:
             (10, 10, 10): "config 1"}.get(tuple(grid), "custom grid")
 
 
+def _config(grid, cycle, ws, dof, nnzb, levels):
+    """The `config` dict of BOTH arms (identical for the same --gpus/--grid/--cycle)."""
+    nx, ny, nz = grid
+    return {"workload": f"SPE10-shaped {nx}x{ny}x{nz} three-phase BSR3 CPR-GMRES solve "
+                        f"({_config_name(grid)}), SolverConfig(theta=0, theta_amg=0, cycle='{cycle}')",
+            "dof": int(dof), "nnz_blocks": int(nnzb), "levels": int(levels),
+            "parallelism": (f"one system row-partitioned into {ws} z-slabs, one GPU each (NCCL halos, "
+                            "GPU-count-invariant reductions, global BILU wavefront over peer memory)")
+            if ws > 1 else "single-gpu",
+            "l2": "working set > 1 GB exceeds the 126 MB L2 (no flush between solves); per-kernel "
+                  "figures flush the L2 before every launch"}
+
+
 def _grid(s):
     return tuple(int(v) for v in s.split(","))
 
@@ -169,6 +184,24 @@ def _time_op(fn, reps, torch):
     e1.record(st)
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / reps * 1e3   # microseconds
+
+
+def _time_cold(fn, reps, torch, flush):
+    """Per-launch device time with the L2 flushed before every launch (a
+    write of a buffer larger than the 126 MB L2 between launches, outside the
+    events): the median over `reps` of cold single launches, microseconds."""
+    st = torch.cuda.current_stream()
+    fn()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(reps)]
+    for e0, e1 in ev:
+        flush.fill_(1.0)
+        e0.record(st)
+        fn()
+        e1.record(st)
+    torch.cuda.synchronize()
+    return float(np.median([e0.elapsed_time(e1) for e0, e1 in ev])) * 1e3
 
 
 def run_ours(args):
@@ -255,37 +288,42 @@ def run_ours(args):
     lvl0 = Bd.amg.levels[0]
     A0 = B.pressure_solver.levels[0].A
     kern = {}
+    warm = {}
     reps = 20
-    us = _time_op(lambda: lib.cprb_spmv(M.desc_ref(), 3, D.ptr(bd), D.ptr(w), None, D.stream()), reps, torch)
-    kern["bsr_spmv"] = (us, _bytes_spmv(nb, nnzb))
+    flush = torch.empty(64 << 20, dtype=torch.float64, device="cuda")     # 512 MB > L2
+
+    def both(name, fn, byt):
+        kern[name] = (_time_cold(fn, reps, torch, flush), byt)
+        warm[name] = _time_op(fn, reps, torch)
+
+    both("bsr_spmv", lambda: lib.cprb_spmv(M.desc_ref(), 3, D.ptr(bd), D.ptr(w), None, D.stream()),
+         _bytes_spmv(nb, nnzb))
     bp = D.empty(A0.nrows)
     xp = D.zeros(A0.nrows)
     bp.copy_(torch.from_numpy(np.ascontiguousarray(b[0::3])).cuda())
-    us = _time_op(lambda: lib.cprb_pgs_scm_pass(C.byref(lvl0.desc), D.ptr(bp), D.ptr(xp), 1, 0,
-                                                D.stream()), reps, torch)
-    kern["pgs_scm_sweep_l0"] = (us, _bytes_sweep(A0.nrows, A0.nnz))
+    both("pgs_scm_sweep_l0", lambda: lib.cprb_pgs_scm_pass(C.byref(lvl0.desc), D.ptr(bp), D.ptr(xp),
+                                                           1, 0, D.stream()),
+         _bytes_sweep(A0.nrows, A0.nnz))
     bc = Bd.amg.levels[1].b if len(Bd.amg.levels) > 1 else D.empty(A0.nrows)
-    us = _time_op(lambda: lib.cprb_resid_restrict(C.byref(lvl0.desc), D.ptr(bp), D.ptr(xp),
-                                                  D.ptr(bc), D.stream()), reps, torch)
-    kern["resid_restrict_l0"] = (us, A0.nnz * 12 + A0.nrows * 28)
+    both("resid_restrict_l0", lambda: lib.cprb_resid_restrict(C.byref(lvl0.desc), D.ptr(bp), D.ptr(xp),
+                                                              D.ptr(bc), D.stream()),
+         A0.nnz * 12 + A0.nrows * 28)
     Fl = B.relaxation
     n_off_l = Fl.L.nnz - nb
     n_off_u = Fl.U.nnz - nb
-    us = _time_op(lambda: Bd.bilu.apply(bd, z), reps, torch)
-    kern["bilu_apply"] = (us, _bytes_bilu(nb, n_off_l, n_off_u))
+    both("bilu_apply", lambda: Bd.bilu.apply(bd, z), _bytes_bilu(nb, n_off_l, n_off_u))
     zp = D.empty(nb)
-    us = _time_op(lambda: N.check(lib.cprb_amg_cycle_graph(Bd.graphs, C.byref(Bd.amg.desc),
-                                                           D.ptr(bd), D.ptr(zp), D.stream())),
-                  reps, torch)
     lv = B.pressure_solver.levels
     vbytes = sum(2 * _bytes_sweep(l.A.nrows, l.A.nnz) + l.A.nnz * 12 + l.A.nrows * 28
                  for l in lv[:-1])
-    kern["amg_vcycle"] = (us, vbytes)
-    us = _time_op(lambda: Bd.apply(bd, z), reps, torch)
-    kern["cpr_apply"] = (us, None)
+    both("amg_vcycle", lambda: N.check(lib.cprb_amg_cycle_graph(Bd.graphs, C.byref(Bd.amg.desc),
+                                                                D.ptr(bd), D.ptr(zp), D.stream())),
+         vbytes)
+    both("cpr_apply", lambda: Bd.apply(bd, z), None)
+    del flush
     kernels = {}
     for k, (us_, byt) in kern.items():
-        d = {"us": round(us_, 2)}
+        d = {"us": round(us_, 2), "us_warm_l2": round(warm[k], 2)}
         if byt:
             gbs = byt / (us_ * 1e-6) / 1e9
             d.update({"bytes": int(byt), "GB/s": round(gbs, 1), "frac": round(gbs / peak, 4)})
@@ -311,13 +349,7 @@ def run_ours(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference generator restated bitwise: seed 0, drift 0.01)",
-        "config": {"workload": f"SPE10-shaped {nx}x{ny}x{nz} three-phase BSR3 CPR-GMRES solve "
-                               f"({_config_name(args.grid)}), SolverConfig(theta=0, theta_amg=0, "
-                               f"cycle='{args.cycle}')",
-                   "dof": n, "nnz_blocks": nnzb, "levels": len(lv),
-                   "parallelism": (f"{ws} independent systems, one per GPU (seed = rank), no "
-                                   "data-path collective") if ws > 1 else "single-gpu",
-                   "l2": "working set > 1 GB exceeds 126 MB L2; no flush"},
+        "config": _config(args.grid, args.cycle, ws, n, nnzb, len(lv)),
         "iters": {"outer": res.outer, "inner": res.inner, "rel_residual": res.rel_residual,
                   "x_err_vs_manufactured": x_err},
         "e2e": {"value": round(e2e_ms, 4), "unit": "ms", "h2d_bytes_per_step": int(8 * n),
@@ -328,6 +360,10 @@ def run_ours(args):
         "gpu_launches_per_solve": launches_per_solve, "kernel_families": kernel_names,
         "clocks": clk.summary(),
     }
+    if ws > 1:
+        out["scaling"] = "weak"
+        out["config"]["parallelism"] = (f"--replicas: {ws} independent systems, one per GPU "
+                                        "(seed = rank), no data-path collective")
     if rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(A, b, args, sample=True)
     if rank == 0:
@@ -336,25 +372,18 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def run_partitioned(args):
-    """Row-slab partitioned solve of ONE system across the N ranks (SURVEY.md
-    8(e); paper_2201_01970_b200/partition.py): strong scaling, NCCL halos +
-    segment all-gathers, levels >= 1 on rank 0, BILU replicated."""
-    import torch
-    import torch.distributed as dist
-
+def _partitioned_record(grid, cycle, steps, warmup, ws, rank, local, torch, dist, clocks=True):
+    """One system row-partitioned over the ws ranks (SURVEY.md 8(e);
+    paper_2201_01970_b200/partition.py): timed solves (max over ranks) and the
+    e2e solve from pinned host buffers.  Returns rank 0's record."""
     import paper_2201_01970_b200 as P
     from paper_2201_01970_b200 import partition as S
 
-    ws, rank, local = _dist()
-    torch.cuda.set_device(local)
-    if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    nx, ny, nz = args.grid
+    nx, ny, nz = grid
     t0 = time.perf_counter()
     (A, b), = P.generate_blackoil_like_sequence(nx, ny, nz, 1, 0.01, 0).systems
     t_gen = time.perf_counter() - t0
-    cfg = P.SolverConfig(theta=0.0, theta_amg=0.0, cycle=args.cycle)
+    cfg = P.SolverConfig(theta=0.0, theta_amg=0.0, cycle=cycle)
     t0 = time.perf_counter()
     B = P.build_cpr(A, cfg)
     comm = S.SlabComm()
@@ -370,8 +399,8 @@ def run_partitioned(args):
     def solve(rhs):
         return S.gmres_solve_slab(A, rhs, None, B, params, comm=comm, part=part, cpr=cpr)
 
-    clk = Clocks(local).__enter__()     # sampler up before the timed region
-    for _ in range(args.warmup):
+    clk = Clocks(local).__enter__() if clocks else None
+    for _ in range(warmup):
         res = solve(bd)
     torch.cuda.synchronize()
     if ws > 1:
@@ -380,15 +409,17 @@ def run_partitioned(args):
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
-    clk.mark(True)
+    if clk:
+        clk.mark(True)
     e0.record(st)
-    for _ in range(args.steps):
+    for _ in range(steps):
         res = solve(bd)
     e1.record(st)
     torch.cuda.synchronize()
-    clk.mark(False)
-    clk.__exit__()
-    ms = e0.elapsed_time(e1) / args.steps
+    if clk:
+        clk.mark(False)
+        clk.__exit__()
+    ms = e0.elapsed_time(e1) / steps
     if ws > 1:
         ms = max_over_ranks(ms, dist, torch, "cuda")
     x = S.gather_rows(res.x, part, comm, 3).cpu().numpy()
@@ -398,7 +429,7 @@ def run_partitioned(args):
     solve(b_pin)                 # warm the pinned result buffers (as run_ours does)
     torch.cuda.synchronize()
     te = []
-    for _ in range(max(1, min(args.steps, 3))):
+    for _ in range(max(1, min(steps, 3))):
         if ws > 1:
             dist.barrier()
         t0 = time.perf_counter()
@@ -411,26 +442,50 @@ def run_partitioned(args):
     launches_per_solve, kernel_names = _count_launches(lambda: solve(bd), torch)
     out = {
         "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": ws,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "steps": steps, "warmup": warmup, "ms_per_step": round(ms, 4),
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference generator restated bitwise: seed 0, drift 0.01)",
-        "config": {"workload": f"SPE10-shaped {nx}x{ny}x{nz} three-phase BSR3 CPR-GMRES solve "
-                               f"({_config_name(args.grid)}), SolverConfig(theta=0, theta_amg=0, "
-                               f"cycle='{args.cycle}')",
-                   "dof": int(b.shape[0]), "nnz_blocks": int(A.nnz),
-                   "parallelism": f"slab-partitioned over {ws} rank(s): NCCL halos + segment "
-                                  "all-gathers; AMG levels >= 1 on rank 0; BILU replicated",
-                   "seg_cells": part.seg_cells,
-                   "l2": "working set > 1 GB exceeds 126 MB L2; no flush"},
+        "config": _config(grid, cycle, ws, b.shape[0], A.nnz, len(B.pressure_solver.levels)),
+        "partition": {"ranks": ws, "seg_cells": part.seg_cells, "bilu": cpr.bilu_mode,
+                      "rows_per_rank": [int(part.rows(q)[1] - part.rows(q)[0]) for q in range(ws)],
+                      "coarse_levels": "levels >= 1 agglomerated on rank 0"},
         "iters": {"outer": res.outer, "inner": res.inner, "rel_residual": res.rel_residual,
                   "x_err_vs_manufactured": x_err},
         "e2e": {"value": round(e2e_ms, 4), "unit": "ms", "h2d_bytes_per_step": int(8 * b_loc.size),
                 "d2h_bytes_per_step": int(8 * b_loc.size)},
         "setup_s": round(t_setup, 2), "generate_s": round(t_gen, 2),
-        "gpu_launches": launches_per_solve * args.steps,
+        "gpu_launches": launches_per_solve * steps,
         "gpu_launches_per_solve": launches_per_solve, "kernel_families": kernel_names,
-        "clocks": clk.summary(),
     }
+    if clk:
+        out["clocks"] = clk.summary()
+    del cpr, B, A
+    return out
+
+
+def run_partitioned(args):
+    """N > 1 default (and --partition at N = 1): the C3 system row-partitioned
+    over the N ranks (strong scaling anchored on the N = 1 BENCH line), plus
+    a config-5 (26.9M DOF) sub-record at the same N (the north star's scaling
+    system; --no-c5 skips it)."""
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    out = _partitioned_record(tuple(args.grid), args.cycle, args.steps, args.warmup, ws, rank,
+                              local, torch, dist)
+    if ws > 1 and not args.no_c5 and tuple(args.grid) == (60, 220, 85):
+        try:
+            torch.cuda.empty_cache()
+            c5 = _partitioned_record((120, 440, 170), args.cycle, max(1, min(args.steps, 5)),
+                                     3, ws, rank, local, torch, dist, clocks=False)
+            out["c5"] = {k: c5[k] for k in ("value", "unit", "steps", "warmup", "config", "partition",
+                                            "iters", "e2e", "setup_s", "gpu_launches_per_solve")}
+        except Exception as exc:  # reported, not fatal: the C3 line above is the bench line
+            out["c5"] = {"error": repr(exc)[:300]}
     if rank == 0:
         print(json.dumps(out))
     if ws > 1:
@@ -588,29 +643,14 @@ def cpu_baseline(A, b, args, sample=True):
             "host_cpus": os.cpu_count()}
 
 
-# Iterations that make up one C3 solve (SURVEY.md section 3(A) and tests/golden/c3_v0.json):
-# 5 inner Arnoldi iterations (CPR apply + BSR SpMV + MGS) + the update application.
-C3_APPLIES_PER_SOLVE = 6
-
-
-def _oracle_iteration(orc, A, B, V, j):
-    """One preconditioned Arnoldi iteration of the oracle's GMRES
-    (src/cpr.py:272-284): z = B v_j, w = A z, MGS against v_0..v_j, normalise."""
-    z = B.apply(V[j])
-    w = orc.spmv(A, z)
-    for i in range(j + 1):
-        h = orc.dot(w, V[i])
-        w = w - h * V[i]
-    hn = orc.norm2(w)
-    return w / hn
-
-
 def run_reference(args):
-    """Reference arm: the reference's CPU algorithm (oracle port; the reference
-    is pure Python and compiles nothing) on the host cores.
-    A full C3 solve takes ~30 s on one core, so each step is a bounded sample
-    of the solve: one preconditioned Arnoldi iteration; the reported value is
-    the per-solve time implied by the solve's iteration structure."""
+    """Reference arm: the reference's CPU algorithm (the oracle port; the
+    reference is pure Python and compiles nothing) on the
+    host cores, for the same workload and config dict as our arm.  Every step
+    (warm-up and timed) is one COMPLETE CPR-GMRES solve of the same system
+    (src/cpr.py:231-316, preconditioner built beforehand as the reference
+    times SETUP and SOLVE separately, src/cpr.py:369-376).  Under torchrun only
+    rank 0 runs; the other ranks exit without work."""
     ws, rank, _ = _dist()
     if rank != 0:
         return
@@ -622,37 +662,46 @@ def run_reference(args):
     t0 = time.perf_counter()
     B = orc.build_cpr(A, cfg)
     t_setup = time.perf_counter() - t0
-    r = b - orc.spmv(A, np.zeros_like(b))
-    V = [r / orc.norm2(r)]
     times = []
     for i in range(args.warmup + args.steps):
-        j = len(V) - 1
         t0 = time.perf_counter()
-        v = _oracle_iteration(orc, A, B, V, j)
+        res = orc.gmres_solve(A, b, None, B, cfg.m, cfg.max_restarts, cfg.tol)
         dt = time.perf_counter() - t0
-        if len(V) < 4:
-            V.append(v)
         if i >= args.warmup:
             times.append(dt)
-    step_ms = float(np.mean(times) * 1e3)
-    ms = step_ms * C3_APPLIES_PER_SOLVE
-    sample = (f"each step = one preconditioned GMRES iteration of the C3 solve on the oracle port "
-              f"(CPR apply + BSR SpMV + MGS, {step_ms:.0f} ms mean); value = "
-              f"{C3_APPLIES_PER_SOLVE} x step (5 inner iterations + the update application of one "
-              f"solve); oracle setup {t_setup:.1f} s untimed; numpy single thread")
+    ms = float(np.mean(times) * 1e3)
+    nlev = len(B.hierarchy.levels)
+    sample = (f"each step = one complete CPR-GMRES solve of the same {b.shape[0]}-DOF system on the "
+              f"oracle port (numpy restatement of cprkit, ~4x faster than the unmodified cprkit "
+              f"package: SURVEY.md 0.3 measured 53.7 s per C3 V solve for cprkit itself); "
+              f"outer={res.outer}, inner={res.inner}, rel={res.rel_residual:.6e}; oracle setup "
+              f"{t_setup:.1f} s untimed; numpy single thread (the reference's path is GIL-bound, "
+              f"pkg/README.md:114-124)")
     out = {"impl": "reference", "metric": METRIC, "value": round(ms, 2), "unit": "ms",
-           "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 2),
-           "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic (reference generator, seed 0, drift 0.01)",
-           "config": {"workload": f"SPE10-shaped {nx}x{ny}x{nz} three-phase BSR3 CPR-GMRES solve "
-                                  f"({_config_name(args.grid)}), SolverConfig(theta=0, theta_amg=0, "
-                                  f"cycle='{args.cycle}')",
-                      "dof": int(b.shape[0])},
+           "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 2),
+           "higher_is_better": False, "scaling": "strong" if ws > 1 else "weak",
+           "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (reference generator restated bitwise: seed 0, drift 0.01)",
+           "config": _config(args.grid, args.cycle, ws, b.shape[0], A.nnz, nlev),
+           "iters": {"outer": res.outer, "inner": res.inner, "rel_residual": res.rel_residual},
            "cpu_baseline": {"value": round(ms, 2), "unit": "ms", "cores": 1, "kind": "port",
                             "sample": sample, "host_cpus": os.cpu_count()},
            "e2e": {"value": round(ms, 2), "unit": "ms", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
+
+
+def _spawn(args) -> int:
+    """--gpus N without torchrun: relaunch this command as N ranks on this
+    node (torch.distributed.run, rendezvous on 127.0.0.1)."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -667,15 +716,23 @@ def main():
     ap.add_argument("--config", default="c3", choices=["c3", "c2", "c4"],
                     help="c2: AMG V-cycle on 128^3 pressure; c4: ASCPR 10-system sequence")
     ap.add_argument("--partition", action="store_true",
-                    help="row-slab partition ONE system over the N ranks (strong scaling)")
+                    help="N = 1: run the row-slab partitioned path (the N > 1 default)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: independent systems per GPU (weak scaling) instead of the partition")
+    ap.add_argument("--no-c5", action="store_true", help="N > 1: skip the config-5 sub-record")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(_spawn(args))
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}")
     if args.impl == "reference":
         run_reference(args)
     elif args.config == "c2":
         run_c2(args)
     elif args.config == "c4":
         run_c4(args)
-    elif args.partition:
+    elif (ws > 1 and not args.replicas) or args.partition:
         run_partitioned(args)
     else:
         run_ours(args)

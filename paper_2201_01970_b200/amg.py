@@ -501,7 +501,8 @@ class DeviceAmg:
             return x
         dl = self.levels[l]
         p = self.h.params
-        x = D.empty(b.shape[0])
+        # zero guess (src/amg.py:250): with pre_sweeps = 0 nothing overwrites x
+        x = D.empty(b.shape[0]) if p.pre_sweeps > 0 else D.zeros(b.shape[0])
         lib, st = N.lib(), D.stream()
         for s in range(p.pre_sweeps):
             N.check(lib.cprb_pgs_scm_pass(C.byref(dl.desc), D.ptr(b), D.ptr(x), 0,

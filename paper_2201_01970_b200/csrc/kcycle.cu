@@ -296,6 +296,10 @@ static int kcycle_at(const KPlan& P, const cprb_amg& h, int l, const double* b, 
   }
   const cprb_amg_level& Lv = h.levels[l];
   int rc;
+  // zero guess (src/amg.py:250): with no pre-sweep nothing overwrites x, and
+  // x is a persistent plan buffer that still holds the previous visit
+  if (P.pre == 0 && cudaMemsetAsync(x, 0, sizeof(double) * (size_t)Lv.n, st) != cudaSuccess)
+    return check_launch("k zero guess");
   for (int sw = 0; sw < P.pre; ++sw)
     if ((rc = pgs_pass(Lv, b, x, 0, sw == 0 ? 1 : 0, nullptr, 0, nullptr, nullptr, st))) return rc;
   double* bc = P.rc[l];

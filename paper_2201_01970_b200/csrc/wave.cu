@@ -487,18 +487,22 @@ static size_t wave_smem(const cprb_wave& W, int b) {
 template <int B, bool UPPER>
 static int launch_wave(const cprb_wave& W, const double* rhs_steps, double* out_step,
                        int32_t* ticket, cudaStream_t st, double* peer_out = nullptr) {
-  static int num_sms = 0;
-  if (!num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  // per-device caches: the SM count and the dynamic-smem opt-in are
+  // properties of the device the launch goes to
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  static int num_sms_dev[64] = {0};
+  if (!num_sms_dev[dev])
+    cudaDeviceGetAttribute(&num_sms_dev[dev], cudaDevAttrMultiProcessorCount, dev);
+  const int num_sms = num_sms_dev[dev];
   if (W.nchunks <= 0) return CPRB_OK;
   const int grid = W.nchunks < num_sms ? W.nchunks : num_sms;
   const size_t smem = wave_smem(W, B);
   // set once per instantiation (the attribute call can serialise against
   // running work; concurrent slab solves on other streams must not wait)
-  static size_t smem_set = 0;
+  static size_t smem_set_dev[64] = {0};
+  size_t& smem_set = smem_set_dev[dev];
   if (smem > smem_set) {
     cudaFuncSetAttribute(k_wave<B, UPPER, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_wave<B, UPPER, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

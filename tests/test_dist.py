@@ -47,3 +47,33 @@ def test_max_over_ranks_gloo_world2():
         assert p.exitcode == 0
     assert [o[0] for o in out] == [0, 1] and all(o[1] == 2 for o in out)
     assert all(o[3] == 15.0 for o in out)          # every rank reports the slowest rank
+
+
+def test_bench_gpus_flag_spawns_ranks():
+    """`bench.py --gpus 2` without torchrun relaunches itself as 2 ranks
+    (torch.distributed.run on 127.0.0.1); the reference arm runs on rank 0
+    only and reports n_gpus = 2 with the same config dict as our arm."""
+    import json
+    import subprocess
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--gpus", "2",
+                          "--grid", "4,4,3", "--steps", "1", "--warmup", "0"],
+                         capture_output=True, text=True, env=env, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    rec = lines[0]
+    assert rec["impl"] == "reference" and rec["n_gpus"] == 2 and rec["scaling"] == "strong"
+    import bench
+    assert rec["config"] == bench._config((4, 4, 3), "v", 2, rec["config"]["dof"],
+                                          rec["config"]["nnz_blocks"], rec["config"]["levels"])
+
+
+def test_bench_gpus_mismatch_is_an_error():
+    import subprocess
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--gpus", "2",
+                          "--grid", "4,4,3", "--steps", "1", "--warmup", "0"],
+                         capture_output=True, text=True, env=env, timeout=300)
+    assert out.returncode != 0 and "WORLD_SIZE" in out.stderr
