@@ -198,6 +198,24 @@ typedef struct cprb_wave {
   int32_t pad_;
 } cprb_wave;
 
+/* Structured-grid ("stencil") BILU(0) plan: the factors of a natural-ordered
+ * nx x ny x nz 7-point grid (exactly the in-range neighbours, so ILU(0)'s L
+ * and U patterns are the -z,-y,-x / +x,+y,+z stencils), stored per xy-plane
+ * in anti-diagonal order (d = ix + iy).  Row (ix, iy, iz) sits at position
+ * iz*P + doff[d] + (ix - lo(d)) (diagonal blocks padded to an even width:
+ * 16-byte TMA granules); its record is contiguous: L 27 doubles, fields
+ * m*9 + e (m: 0 -z, 1 -y, 2 -x; e = r*3 + c), U 37 doubles, fields m*9 + e
+ * (m: 0 +x, 1 +y, 2 +z), the 9 entries of inv(U_ii), one pad word. */
+typedef struct cprb_stencil {
+  int32_t nx, ny, nz;          /* grid (x fastest) */
+  int32_t S;                   /* x-segments of 32 lanes (ceil(nx / 32) <= 4) */
+  int32_t D;                   /* anti-diagonals per plane (nx + ny - 1) */
+  int32_t P;                   /* padded rows per plane (doff[D]) */
+  const int32_t* doff;         /* dev, D + 1 padded diagonal offsets */
+  const double* lrec;          /* dev, nz * P * 27 */
+  const double* urec;          /* dev, nz * P * 37 */
+} cprb_stencil;
+
 typedef struct cprb_bilu {
   int32_t n;                   /* block rows */
   int32_t b;                   /* block size (1 or 3) */
@@ -205,7 +223,7 @@ typedef struct cprb_bilu {
   cprb_sell U;                 /* strict upper blocks; lanes in U-level order */
   const double* uinv;          /* dev, U lane layout: [(s*b*b + e)*32 + l] */
   int32_t* tickets;            /* dev, 4 ints (dynamic warp / chunk ordering) */
-  int32_t use_wave;            /* 1: chunked-wavefront kernels (Lw/Uw) */
+  int32_t use_wave;            /* 1: chunked-wavefront kernels (Lw/Uw); 2: stencil plan (St) */
   cprb_wave Lw;
   cprb_wave Uw;
   const int32_t* l_slot;       /* dev, n: rhs slot of each row in the L plan */
@@ -216,6 +234,7 @@ typedef struct cprb_bilu {
   double* y_step;              /* dev work: y in U step order (U output, sentinel-polled) */
   int64_t len_l;               /* doubles in rhs_l / zl_step */
   int64_t len_u;               /* doubles in rhs_u / y_step */
+  cprb_stencil St;             /* use_wave == 2: l_slot == u_slot = 3 * stencil position */
 } cprb_bilu;
 
 typedef struct cprb_cpr {
@@ -275,6 +294,10 @@ int cprb_bilu_apply(const cprb_bilu* F, const double* r, double* z, double* work
 /* Diagnostic: record per-step completion times of the wave solves into
  * dev_log ([2][256 chunks][512 steps] uint64, %globaltimer); NULL = off. */
 int cprb_wave_set_log(uint64_t* dev_log);
+/* Diagnostic: per-plane timeline of the stencil BILU solves ([2][1024 planes]
+ * x 8 u64: start/end %globaltimer, cycles in TMA waits, cycles in plane
+ * waits, total cycles, diagonals); NULL = off. */
+int cprb_stencil_set_log(uint64_t* dev_log);
 /* Diagnostic: V-cycle kernel timeline ({kind, start, after-wait, end} u64 per
  * launch, %globaltimer, <= 4096 launches); resets the counter; NULL = off. */
 int cprb_amg_set_log(uint64_t* dev_log);

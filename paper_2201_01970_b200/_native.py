@@ -63,11 +63,16 @@ class Wave(C.Structure):
                 ("stream", vp), ("max_chunk_steps", C.c_int32), ("pad_", C.c_int32)]
 
 
+class Stencil(C.Structure):
+    _fields_ = [("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32), ("S", C.c_int32),
+                ("D", C.c_int32), ("P", C.c_int32), ("doff", vp), ("lrec", vp), ("urec", vp)]
+
+
 class Bilu(C.Structure):
     _fields_ = [("n", C.c_int32), ("b", C.c_int32), ("L", Sell), ("U", Sell), ("uinv", vp),
                 ("tickets", vp), ("use_wave", C.c_int32), ("Lw", Wave), ("Uw", Wave),
                 ("l_slot", vp), ("rhs_l", vp), ("rhs_u", vp), ("u_slot", vp), ("zl_step", vp),
-                ("y_step", vp), ("len_l", C.c_int64), ("len_u", C.c_int64)]
+                ("y_step", vp), ("len_l", C.c_int64), ("len_u", C.c_int64), ("St", Stencil)]
 
 
 class Cpr(C.Structure):
@@ -95,6 +100,7 @@ _SIGS = {
     "cprb_bilu_apply": (C.c_int, [C.POINTER(Bilu), vp, vp, vp, vp]),
     "cprb_cpr_apply": (C.c_int, [C.POINTER(Cpr), vp, vp, vp]),
     "cprb_wave_set_log": (C.c_int, [vp]),
+    "cprb_stencil_set_log": (C.c_int, [vp]),
     "cprb_pack_bsr_sell": (C.c_int, [C.c_int64, C.c_int32, vp, vp, vp, vp, vp, vp, vp]),
     "cprb_kcycle_create": (C.c_int, [vp, vp, C.c_int32, C.c_int32, vp]),
     "cprb_kcycle_destroy": (C.c_int, [vp]),

@@ -192,7 +192,7 @@ extern "C" int cprb_bilu_apply(const cprb_bilu* F, const double* r, double* z, d
     if (rc) return rc;
     rc = wave_scatter_rhs(*F, r, F->rhs_l, st);
     if (rc) return rc;
-    rc = wave_solve(*F, F->rhs_l, st);
+    rc = F->use_wave == 2 ? stencil_solve(*F, F->rhs_l, st) : wave_solve(*F, F->rhs_l, st);
     if (rc) return rc;
     return wave_combine(*F, nullptr, z, st);
   }

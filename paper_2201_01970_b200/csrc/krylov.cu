@@ -234,7 +234,7 @@ int cprb_cpr_finish(const cprb_cpr* P, const double* r, double* z, void* stream)
     if (rc) return rc;
     // the solves publish in step order (coalesced); z = Pi zp + y is one
     // gather pass afterwards
-    rc = wave_solve(F, F.rhs_l, st);
+    rc = F.use_wave == 2 ? stencil_solve(F, F.rhs_l, st) : wave_solve(F, F.rhs_l, st);
     if (rc) return rc;
     return wave_combine(F, P->zp, z, st);
   }

@@ -313,6 +313,78 @@ def wave_plan(T: BlockCsrMatrix, sched: LevelSchedule, b: int, upper: bool, uinv
     return host, rhs_slot
 
 
+STENCIL_SMAX = 4   # x-segments of 32 lanes per warp (csrc/stencil.cu): nx <= 128
+
+
+def stencil_plan(F: BiluFactors):
+    """Structured-grid plan of the BILU(0) solves (csrc/stencil.cu), or None.
+
+    Applies when the factors are those of a natural-ordered nx x ny x nz
+    7-point grid with every in-range neighbour present (the reference
+    generator's Jacobians, src/problems.py:57-155): the strict-lower pattern
+    of row (ix, iy, iz) is exactly {-z, -y, -x} in range, the strict-upper
+    pattern {+x, +y, +z}.  Rows are laid out per xy-plane in anti-diagonal
+    order d = ix + iy (diagonal blocks padded to an even width), each
+    row's factor record contiguous (row-major): L fields m*9 + e (m: -z, -y,
+    -x), U fields m*9 + e (m: +x, +y, +z) then inv(U_ii) and one pad word.
+    Absent neighbours (grid faces) are zero-filled and masked by the kernel."""
+    b, n = F.block_size, F.n
+    if b != 3 or n < 2:
+        return None
+    lp, lc, lv = _strict(F.L)
+    up, uc, uv = _strict(F.U)
+    rows_l = np.repeat(np.arange(n, dtype=np.int64), np.diff(lp))
+    offs = np.unique(rows_l - lc)
+    if offs.shape[0] != 3 or offs[0] != 1:
+        return None
+    nx, nxy = int(offs[1]), int(offs[2])
+    if nx < 2 or nxy % nx or n % nxy or nxy // nx < 2:
+        return None
+    ny, nz = nxy // nx, n // nxy
+    if nz < 2 or nx > 32 * STENCIL_SMAX:
+        return None
+    i = np.arange(n, dtype=np.int64)
+    ix, iy, iz = i % nx, (i // nx) % ny, i // nxy
+    # exact stencil patterns in ascending column order
+    hl = np.stack([iz > 0, iy > 0, ix > 0], axis=1)
+    hu = np.stack([ix < nx - 1, iy < ny - 1, iz < nz - 1], axis=1)
+    if not (np.array_equal(np.diff(lp), hl.sum(1)) and np.array_equal(np.diff(up), hu.sum(1))):
+        return None
+    ol = np.array([nxy, nx, 1], dtype=np.int64)
+    ou = np.array([1, nx, nxy], dtype=np.int64)
+    exp_l = (i[:, None] - ol[None, :])[hl]
+    exp_u = (i[:, None] + ou[None, :])[hu]
+    if not (np.array_equal(exp_l, lc) and np.array_equal(exp_u, uc)):
+        return None
+    Dn = nx + ny - 1
+    d = np.arange(Dn, dtype=np.int64)
+    lo = np.maximum(0, d - (ny - 1))
+    hi = np.minimum(nx - 1, d)
+    w = hi - lo + 1
+    wp = w + (w & 1)
+    doff = np.zeros(Dn + 1, dtype=np.int64)
+    np.cumsum(wp, out=doff[1:])
+    P = int(doff[-1])
+    dc = ix + iy
+    j = ix - lo[dc]
+    pos = iz * P + doff[dc] + j                       # stencil position of every row
+
+    def records(vals, mask, nf, extra=None):
+        # row-major per stencil position: fields m*9 + e, then `extra`
+        rec = np.zeros((nz * P, nf))
+        r_of, m_of = np.nonzero(mask)
+        rec[pos[r_of][:, None], (m_of * 9)[:, None] + np.arange(9)[None, :]] = vals.reshape(-1, 9)
+        if extra is not None:
+            rec[pos, 27:36] = extra.reshape(-1, 9)
+        return rec.reshape(-1)
+
+    lrec = records(lv, hl, 27)
+    urec = records(uv, hu, 37, F.u_diag_inv)       # 36 + 1 pad (bank-conflict-free stride)
+    return {"nx": nx, "ny": ny, "nz": nz, "S": (nx + 31) // 32, "D": Dn, "P": P,
+            "doff": doff.astype(np.int32), "lrec": lrec, "urec": urec,
+            "slot": (3 * pos).astype(np.int32), "len": 3 * nz * P}
+
+
 class WaveDev:
     def __init__(self, host):
         self.host = host
@@ -336,6 +408,10 @@ class DeviceBilu:
         if b not in (1, 3):
             raise NotImplementedError(f"device BILU supports block sizes 1 and 3, got {b}")
         self.use_wave = bool(F.n > 0 and use_wave)
+        st = None
+        if self.use_wave and os.environ.get("CPRB_STENCIL", "1") != "0":
+            st = stencil_plan(F)
+        self.stencil = st is not None
         if self.use_wave:
             # the wave plans carry their own copies of the factors; the
             # level-ordered SELL-32 layout is only built for the sync-free variant
@@ -353,7 +429,26 @@ class DeviceBilu:
         self.tickets = t.zeros(8, dtype=t.int32, device="cuda")
         self.work = D.empty(max(F.n * b, 1))
         self.n, self.b = F.n, b
-        if self.use_wave:
+        stdesc = N.Stencil()
+        if st is not None:
+            # structured grid: one warp per xy-plane sweeping anti-diagonals
+            # (csrc/stencil.cu); rhs, L output and U output share the layout
+            self.Lw = self.Uw = None
+            self.st_doff = D.upload(st["doff"])
+            self.st_lrec = D.upload(st["lrec"])
+            self.st_urec = D.upload(st["urec"])
+            self.l_slot = self.u_slot = D.upload(st["slot"])
+            self.len_l = self.len_u = max(int(st["len"]), 1)
+            self.rhs_l = D.zeros(self.len_l)
+            self.rhs_u = self.rhs_l
+            self.zl_step = D.zeros(self.len_l)
+            self.y_step = D.zeros(self.len_u)
+            extra = (D.ptr(self.l_slot), D.ptr(self.rhs_l), D.ptr(self.rhs_u), D.ptr(self.u_slot),
+                     D.ptr(self.zl_step), D.ptr(self.y_step), self.len_l, self.len_u)
+            wl, wu = N.Wave(), N.Wave()
+            stdesc = N.Stencil(st["nx"], st["ny"], st["nz"], st["S"], st["D"], st["P"],
+                               D.ptr(self.st_doff), D.ptr(self.st_lrec), D.ptr(self.st_urec))
+        elif self.use_wave:
             hu, uslot = wave_plan(F.U, F.u_schedule, b, True, uinv=F.u_diag_inv)
             hl, lslot = wave_plan(F.L, F.l_schedule, b, False)
             self.Lw, self.Uw = WaveDev(hl), WaveDev(hu)
@@ -371,7 +466,8 @@ class DeviceBilu:
             wl, wu = N.Wave(), N.Wave()
             extra = (0, 0, 0, 0, 0, 0, 0, 0)
         self.desc = N.Bilu(F.n, b, ldesc, udesc, uptr, D.ptr(self.tickets),
-                           1 if self.use_wave else 0, wl, wu, *extra)
+                           (2 if self.stencil else 1) if self.use_wave else 0, wl, wu, *extra,
+                           stdesc)
 
     def apply(self, r, z):
         N.check(N.lib().cprb_bilu_apply(C.byref(self.desc), D.ptr(r), D.ptr(z), D.ptr(self.work),
