@@ -506,17 +506,23 @@ def test_c4_sequence_reuse_against_survey(gpu):
 
 @pytest.mark.slow
 def test_spe10_shape_c3_kcycle_against_reference(gpu):
-    """Config 3 with the K-cycle (nonlinear AMLI, FCG on the symmetric A_PP):
-    the reference run of SURVEY.md section 0.3 took outer 2 / inner 5 with a
-    final relative residual of 2.131596607608327e-06 and ||x - x*|| / ||x*||
-    = 4.78e-6 (the explicit-residual restart must be reproduced, not fixed)."""
+    """Config 3 with the K-cycle (nonlinear AMLI, FCG on the symmetric A_PP),
+    against the unmodified reference's run recorded in tests/golden/c3_k0.json
+    (make_golden.py --bigk): outer 2 / inner 5 with the explicit-residual
+    restart reproduced, the Givens history of both cycles within 1e-8, the
+    solution samples within 1e-6 and ||x - x*|| / ||x*|| = 4.78e-6."""
+    ref = json.loads((GOLDEN / "c3_k0.json").read_text())
     (A, b), = P.generate_blackoil_like_sequence(60, 220, 85, 1, 0.01, 0).systems
     cfg = P.SolverConfig(theta=0.0, theta_amg=0.0, cycle="k")
     B = P.build_cpr(A, cfg)
     assert B.pressure_solver.symmetric
-    res = P.gmres_solve(A, b, None, B, cfg.gmres_params())
-    assert (res.outer, res.inner, res.converged) == (2, 5, True)
-    assert abs(res.rel_residual - 2.131596607608327e-06) <= 1e-8 * 2.131596607608327e-06
+    res = P.gmres_solve(A, b, None, B, cfg.gmres_params(), history=True)
+    assert (res.outer, res.inner, res.converged) == (ref["outer"], ref["inner"], True) == (2, 5, True)
+    hist = np.array([hh if not isinstance(hh, tuple) else -hh[1] for hh in res.history])
+    np.testing.assert_allclose(hist, ref["hist"], rtol=1e-8)
+    assert abs(res.rel_residual - ref["rel"]) <= 1e-8 * ref["rel"]
+    xs_ref = np.asarray(ref["x_sample"])
+    assert np.linalg.norm(res.x[::ref["x_sample_stride"]] - xs_ref) <= 1e-6 * np.linalg.norm(xs_ref)
     xs = P.problems.manufactured_solution(60 * 220 * 85)
     err = np.linalg.norm(res.x - xs) / np.linalg.norm(xs)
     assert abs(err - 4.78e-6) <= 0.01e-6
