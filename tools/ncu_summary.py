@@ -2,7 +2,11 @@
 profiles/<round>_ncu_summary.md and profiles/ncu_traffic.json (the DRAM
 traffic per launch that bench.py reports as roofline.traffic).
 
-    python tools/ncu_summary.py r01
+    python tools/ncu_summary.py r01            # gpurun_out/final_*.ncu-rep
+    python tools/ncu_summary.py r02            # gpurun_out/r02_*.ncu-rep
+
+Families already in profiles/ncu_traffic.json that this round did not
+re-capture are kept.
 """
 import csv
 import io
@@ -49,9 +53,12 @@ lines = [f"# {tag}: ncu --set full captures of the committed kernels (C3, 1 B200
          "| kernel | grid x block | time us | DRAM read MB | DRAM write MB | DRAM % of peak | warps active % | regs | L2 hit % |",
          "|---|---|---|---|---|---|---|---|---|"]
 traffic = {}
-for f in ["final_bsr", "final_sweep", "final_rr", "final_wave"]:
-    rep = OUT / f"{f}.ncu-rep"
-    if not rep.exists():
+FAMILY = {"bsr": "bsr_spmv", "sweep": "pgs_scm_sweep_l0", "rr": "resid_restrict_l0",
+          "wave": "bilu_apply", "stencil": "bilu_apply", "ktail": "kcycle_tail"}
+prefix = "final" if tag == "r01" else tag
+for rep in sorted(OUT.glob(f"{prefix}_*.ncu-rep")):
+    f = rep.stem[len(prefix) + 1:]
+    if f not in FAMILY:
         continue
     for d in raw(rep):
         lines.append(f"| {d['name']} | {d.get('launch__grid_size'):.0f} x {d.get('launch__block_size'):.0f} | "
@@ -60,8 +67,7 @@ for f in ["final_bsr", "final_sweep", "final_rr", "final_wave"]:
                      f"{d['gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed']:.1f} | "
                      f"{d['sm__warps_active.avg.pct_of_peak_sustained_active']:.1f} | "
                      f"{d['launch__registers_per_thread']:.0f} | {d['lts__t_sector_hit_rate.pct']:.1f} |")
-        fam = {"final_bsr": "bsr_spmv", "final_sweep": "pgs_scm_sweep_l0", "final_rr": "resid_restrict_l0",
-               "final_wave": "bilu_apply"}[f]
+        fam = FAMILY[f]
         b = d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"]
         traffic.setdefault(fam, {"dram_bytes": 0, "launches": 0})
         traffic[fam]["dram_bytes"] += b
@@ -69,7 +75,7 @@ for f in ["final_bsr", "final_sweep", "final_rr", "final_wave"]:
 # the sweep capture holds the two level-0 colour launches of one pass; wave holds L + U
 for fam in traffic:
     traffic[fam]["dram_bytes"] = int(traffic[fam]["dram_bytes"])
-lst = OUT / "launches_solve_final.csv"
+lst = OUT / ("launches_solve_final.csv" if tag == "r01" else f"launches_solve_{tag}.csv")
 if lst.exists():
     rows = list(csv.reader(open(lst)))
     hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
@@ -90,8 +96,12 @@ if lst.exists():
     for k, v in sorted(tot.items(), key=lambda x: -x[1])[:16]:
         lines.append(f"| {k} | {cnt[k]} | {v:.0f} | {v / T * 100:.1f}% |")
 (ROOT / "profiles" / f"{tag}_ncu_summary.md").write_text("\n".join(lines) + "\n")
-(ROOT / "profiles" / "ncu_traffic.json").write_text(json.dumps(
-    {"source": f"profiles/{tag}_ncu_summary.md (ncu --set full, dram__bytes_read.sum + "
-               "dram__bytes_write.sum per launch group)", "grid": [60, 220, 85], "kernels": traffic},
-    indent=1) + "\n")
+tj = ROOT / "profiles" / "ncu_traffic.json"
+old = json.loads(tj.read_text()) if tj.exists() else {"kernels": {}}
+for fam, v in traffic.items():
+    v["source"] = f"profiles/{tag}_ncu_summary.md"
+    old["kernels"][fam] = v
+old.update({"source": "ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum per launch "
+                      "group (per-family source file)", "grid": [60, 220, 85]})
+tj.write_text(json.dumps(old, indent=1) + "\n")
 print("\n".join(lines))
