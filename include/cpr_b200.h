@@ -81,6 +81,16 @@ int cprb_bilu0_factorize(int64_t n, int32_t b, const int64_t* ptr, const int64_t
 int cprb_level_schedule(int64_t n, const int64_t* ptr, const int64_t* cols,
                         int64_t* level, int64_t* nlevels);
 
+/* src/ilu.py:38-59 applied to the strict lower part of A's own pattern (the
+ * BILU(0) factorization's row dependencies).  level[n], *nlevels. */
+int cprb_lower_level_schedule(int64_t n, const int64_t* ptr, const int64_t* cols,
+                              int64_t* level, int64_t* nlevels);
+
+/* Structured 7-point grid test for the stencil BILU plan: returns 1 and
+ * dims[3] = {nx, ny, nz} when every row's block columns are exactly the
+ * in-range neighbours of a natural-ordered grid (nx, ny, nz >= 2), else 0. */
+int cprb_detect_stencil(int64_t n, const int64_t* ptr, const int64_t* cols, int64_t* dims);
+
 /* coarsest level (replaces scipy lu_factor/lu_solve, src/amg.py:170-173,
  * :248-249): dense inverse via LU with partial pivoting; a: n*n row-major. */
 int cprb_dense_inverse(int64_t n, const double* a, double* inv);
@@ -124,25 +134,8 @@ typedef struct cprb_amg_level {
   double* tmp;                 /* dev work, n (snapshot sweeps) */
   const int32_t* color_width;  /* host|NULL, 2*ncolors: max lane_len, max lane_len_lo per colour */
   int32_t restrict_width;      /* max row length of restrict_op (0 = unknown) */
-  int32_t one_cta;             /* 1 = V-cycle runs this level's passes in one CTA (x in smem) */
-} cprb_amg_level;
-
-/* Device pointers of one coarse level for the persistent V-cycle tail
- * (csrc/amg.cu: k_vtail3); the tail's static data itself is packed per CTA
- * (tail3_buf).  color_off is unused (0). */
-typedef struct cprb_tail_level {
-  cprb_sell smoother;
-  cprb_sell restrict_op;
-  const double* diag;
-  const int32_t* aggp;
-  double* b;
-  double* x;
-  double* tmp;
-  int32_t n;
-  int32_t ncolors;
-  int32_t color_off;
   int32_t pad_;
-} cprb_tail_level;
+} cprb_amg_level;
 
 typedef struct cprb_amg {
   int32_t nlevels;                  /* total, including the coarsest */
@@ -157,19 +150,20 @@ typedef struct cprb_amg {
   int32_t use_fcg;                  /* K-cycle Krylov flavour */
   void* kwork;                       /* K-cycle plan (cprb_kcycle_create) or NULL; used when cycle = 1 */
   int64_t kwork_len;
-  /* persistent tail: levels >= tail_start (and the coarse solve) run in one
-   * cluster-wide kernel; tail_start >= nlevels-1 disables it. */
+  /* persistent single-CTA V-cycle tail (csrc/vtail.cu): levels >= tail_start
+   * and the coarse solve in one launch, vectors in shared memory, static
+   * records streamed by TMA; tail_start >= nlevels-1 disables it. */
   int32_t tail_start;
-  int32_t tail_ctas;                /* cluster size (1..16) */
-  const cprb_tail_level* tail_levels; /* dev, nlevels-1 entries (index = level) */
-  const int32_t* tail_colors;       /* unused (0) */
-  const int32_t* tail_phases;       /* dev, tail_nphases x {type, level, colour, flags} */
   int32_t tail_nphases;
-  int32_t tail_mode;                /* 3: shared-memory-resident cluster tail; 0: off */
-  const uint8_t* tail3_buf;         /* dev: per-CTA packed static data (mode 3) */
-  const int64_t* tail3_seg;         /* dev: [ctas][nphases+1] byte offsets into tail3_buf */
-  int32_t tail3_max_bytes;          /* largest per-CTA buffer (dynamic shared memory) */
-  int32_t pad2_;
+  int32_t tail_nchunks;
+  int32_t tail_slot;                /* ring slot bytes (multiple of 16) */
+  int32_t tail_smem;                /* dynamic shared memory bytes of the launch */
+  int32_t tail_vec_len;             /* doubles of the shared-memory vector region */
+  const int32_t* tail_phases;       /* dev, (nphases+1) x {type, level, colour|zg, first chunk} */
+  const int32_t* tail_chunks;       /* dev, nchunks x {phase, 16-byte offset, bytes, rows} */
+  const uint8_t* tail_stream;       /* dev, packed chunk records */
+  const int32_t* tail_vec;          /* dev, 2*nlevels: shared-memory offsets of b_l, x_l */
+  int64_t tail_stream_bytes;        /* bytes of tail_stream (L2 persistence window) */
 } cprb_amg;
 
 /* Chunked-wavefront plan of one triangular factor (csrc/wave.cu).  Rows are
@@ -251,6 +245,31 @@ typedef struct cprb_cpr {
 
 /* ============================ device kernels ============================ */
 
+/* SETUP on the device.  src/ilu.py:150-193 BILU(0) of a 3x3-block matrix in
+ * place on A's pattern (dev ptr/cols int64, vals n_blocks*9), uinv[n*9] =
+ * inverted pivots; rows are processed level by level (level_rows: dev int32,
+ * rows grouped by cprb_lower_level_schedule level; level_ptr: HOST int64,
+ * nlevels+1).  err: dev int32[4] -> {lowest zero-pivot row, lowest row
+ * without a diagonal block (INT32_MAX = none), number of perturbed pivots};
+ * perturbed: dev int64[n] (unordered).  Bitwise the host factorization. */
+int cprb_bilu0_factorize_device(int64_t n, int32_t b, const int64_t* ptr, const int64_t* cols,
+                                double* vals, double* uinv, const int32_t* level_rows,
+                                const int64_t* level_ptr, int64_t nlevels, int32_t* err,
+                                int64_t* perturbed, void* stream);
+/* Factored CSR (A's pattern) -> stencil records (cprb_stencil lrec/urec,
+ * zero-initialised by the caller) and the per-row rhs slot (3 * position). */
+int cprb_stencil_pack(int64_t n, int32_t nx, int32_t ny, int32_t P, const int32_t* doff,
+                      const int64_t* ptr, const int64_t* cols, const double* vals,
+                      const double* uinv, double* lrec, double* urec, int32_t* slot,
+                      void* stream);
+/* src/problems.py:113-155 on the device (nx*ny*nz cells, 3x3 blocks):
+ * row counts, then the rows (int64 block columns ascending, 9 values per
+ * block) given the host-drawn perm = exp(logk), conv_scale and couple[n*6]. */
+int cprb_gen_row_counts(int64_t nx, int64_t ny, int64_t nz, int64_t* cnt, void* stream);
+int cprb_gen_assemble(int64_t nx, int64_t ny, int64_t nz, double drift, const double* perm,
+                      const double* conv_scale, const double* couple, const int64_t* row_ptr,
+                      int64_t* cols, double* vals, void* stream);
+
 /* src/sparse.py:335-351  y = A x (BSR via the expanded-row order).  flag
  * (dev|NULL) is set to 1 when any y is non-finite. */
 int cprb_spmv(const cprb_sell* A, int32_t b, const double* x, double* y, int32_t* flag,
@@ -298,11 +317,12 @@ int cprb_wave_set_log(uint64_t* dev_log);
  * x 8 u64: start/end %globaltimer, cycles in TMA waits, cycles in plane
  * waits, total cycles, diagonals); NULL = off. */
 int cprb_stencil_set_log(uint64_t* dev_log);
+/* Diagnostic: persistent V-cycle tail timeline (consumer thread 0: start,
+ * after the PDL wait, then the end of every phase; u64 %globaltimer). */
+int cprb_vtail_set_log(uint64_t* dev_log);
 /* Diagnostic: V-cycle kernel timeline ({kind, start, after-wait, end} u64 per
  * launch, %globaltimer, <= 4096 launches); resets the counter; NULL = off. */
 int cprb_amg_set_log(uint64_t* dev_log);
-/* Diagnostic: per-phase end times of the smem-resident tail (CTA 0); NULL = off. */
-int cprb_tail3_set_log(uint64_t* dev_log);
 
 /* src/cpr.py:178-186  z = B r (V-cycle pressure stage). */
 int cprb_cpr_apply(const cprb_cpr* P, const double* r, double* z, void* stream);

@@ -36,13 +36,7 @@ class AmgLevel(C.Structure):
                 ("color_rows", i32p), ("color_snapshot", u8p), ("smoother", Sell),
                 ("diag", vp), ("restrict_op", Sell), ("aggp", vp), ("b", vp), ("x", vp),
                 ("tmp", vp), ("color_width", i32p), ("restrict_width", C.c_int32),
-                ("one_cta", C.c_int32)]
-
-
-class TailLevel(C.Structure):
-    _fields_ = [("smoother", Sell), ("restrict_op", Sell), ("diag", vp), ("aggp", vp), ("b", vp),
-                ("x", vp), ("tmp", vp), ("n", C.c_int32), ("ncolors", C.c_int32),
-                ("color_off", C.c_int32), ("pad_", C.c_int32)]
+                ("pad_", C.c_int32)]
 
 
 class Amg(C.Structure):
@@ -50,10 +44,10 @@ class Amg(C.Structure):
                 ("coarse_inv", vp), ("coarse_b", vp), ("coarse_x", vp), ("perm0", vp),
                 ("in_stride", C.c_int32), ("cycle", C.c_int32), ("use_fcg", C.c_int32),
                 ("kwork", vp), ("kwork_len", C.c_int64), ("tail_start", C.c_int32),
-                ("tail_ctas", C.c_int32), ("tail_levels", vp), ("tail_colors", vp),
-                ("tail_phases", vp), ("tail_nphases", C.c_int32), ("tail_mode", C.c_int32),
-                ("tail3_buf", vp), ("tail3_seg", vp), ("tail3_max_bytes", C.c_int32),
-                ("pad2_", C.c_int32)]
+                ("tail_nphases", C.c_int32), ("tail_nchunks", C.c_int32), ("tail_slot", C.c_int32),
+                ("tail_smem", C.c_int32), ("tail_vec_len", C.c_int32), ("tail_phases", vp),
+                ("tail_chunks", vp), ("tail_stream", vp), ("tail_vec", vp),
+                ("tail_stream_bytes", C.c_int64)]
 
 
 class Wave(C.Structure):
@@ -102,6 +96,16 @@ _SIGS = {
     "cprb_wave_set_log": (C.c_int, [vp]),
     "cprb_stencil_set_log": (C.c_int, [vp]),
     "cprb_pack_bsr_sell": (C.c_int, [C.c_int64, C.c_int32, vp, vp, vp, vp, vp, vp, vp]),
+    "cprb_lower_level_schedule": (C.c_int, [C.c_int64, vp, vp, vp, vp]),
+    "cprb_detect_stencil": (C.c_int, [C.c_int64, vp, vp, vp]),
+    "cprb_bilu0_factorize_device": (C.c_int, [C.c_int64, C.c_int32, vp, vp, vp, vp, vp, vp,
+                                              C.c_int64, vp, vp, vp]),
+    "cprb_stencil_pack": (C.c_int, [C.c_int64, C.c_int32, C.c_int32, C.c_int32, vp, vp, vp, vp,
+                                    vp, vp, vp, vp, vp]),
+    "cprb_vtail_set_log": (C.c_int, [vp]),
+    "cprb_gen_row_counts": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, vp, vp]),
+    "cprb_gen_assemble": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_double, vp, vp, vp, vp,
+                                    vp, vp, vp]),
     "cprb_kcycle_create": (C.c_int, [vp, vp, C.c_int32, C.c_int32, vp]),
     "cprb_kcycle_destroy": (C.c_int, [vp]),
     "cprb_kcycle_correction": (C.c_int, [vp, C.c_int32, vp, vp, vp, vp]),
@@ -120,7 +124,6 @@ _SIGS = {
     "cprb_unpad": (C.c_int, [C.c_int32, C.c_int64, vp, vp, vp, vp]),
     "cprb_cpr_combine": (C.c_int, [C.c_int64, C.c_int32, vp, vp, vp, vp]),
     "cprb_amg_set_log": (C.c_int, [vp]),
-    "cprb_tail3_set_log": (C.c_int, [vp]),
     "cprb_coarse_solve": (C.c_int, [C.POINTER(Amg), vp, vp, vp]),
     "cprb_resid_restrict": (C.c_int, [C.POINTER(AmgLevel), vp, vp, vp, vp]),
     "cprb_prolong": (C.c_int, [C.POINTER(AmgLevel), vp, vp, vp]),

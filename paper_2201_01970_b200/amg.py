@@ -143,36 +143,76 @@ def _dense_inverse(A) -> np.ndarray:
     return inv
 
 
+_POOL = None
+
+
+def setup_pool():
+    """Host thread pool of the SETUP phase.  The C++ setup kernels are called
+    through ctypes (the GIL is released) and the numpy passes release it for
+    large arrays, so independent pieces of setup run concurrently."""
+    global _POOL
+    if _POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+        n = int(os.environ.get("CPRB_SETUP_THREADS", str(min(16, os.cpu_count() or 1))))
+        _POOL = ThreadPoolExecutor(max_workers=max(1, n), thread_name_prefix="cprb-setup")
+    return _POOL
+
+
+def _smooth_level(A_l, params):
+    partition = vertices_grouping(strong_connections(A_l, params.smoother_theta))
+    spec = SmootherSpec(kind=params.smoother_kind,
+                        partition=partition if params.smoother_kind == "pgs-scm" else None)
+    return partition, make_smoother(A_l, spec)
+
+
 def build_hierarchy(A_p, params: AmgParams | None = None) -> AmgHierarchy:
     """src/amg.py:143-174: aggregate / project until the coarsest target, the
-    level cap or a coarsening stall (n_agg > 0.9 n)."""
+    level cap or a coarsening stall (n_agg > 0.9 n).
+
+    The aggregation -> Galerkin chain is sequential; each level's colouring
+    and smoother depend only on that level's matrix and are built on the
+    setup pool while the chain continues.  Errors surface in the reference's
+    order: a level's smoother error before anything later in the chain."""
     params = params or AmgParams()
     if A_p.nrows != A_p.ncols:
         raise ValueError("hierarchy needs a square matrix")
     if not isinstance(A_p, CsrMatrix):
         A_p = CsrMatrix(A_p.nrows, A_p.ncols, A_p.row_ptr, A_p.col_idx, A_p.values)
+    pool = setup_pool()
+    pending = []          # (level index, A_l, agg, future)
     levels = []
     A_l = A_p
-    sym = _is_symmetric(A_p)
-    while True:
-        if A_l.nrows <= params.coarsest_size or len(levels) + 1 >= params.max_levels:
-            levels.append(AmgLevel(A_l, None, None))
-            break
-        agg = pairwise_aggregate(A_l, params.theta_amg)
-        if agg.n_aggregates > 0.9 * A_l.nrows:
-            levels.append(AmgLevel(A_l, None, None))
-            break
-        partition = vertices_grouping(strong_connections(A_l, params.smoother_theta))
-        spec = SmootherSpec(kind=params.smoother_kind,
-                            partition=partition if params.smoother_kind == "pgs-scm" else None)
-        smoother = make_smoother(A_l, spec)
-        levels.append(AmgLevel(A_l, partition, smoother, P=_prolongation(agg, A_l.nrows),
-                               aggregates=agg.aggregate_of))
-        A_l = _galerkin(A_l, agg)
+
+    def first_smoother_error():
+        for _, _, _, fut in pending:
+            exc = fut.exception()
+            if exc is not None:
+                return exc
+        return None
+
     try:
-        inv = _dense_inverse(levels[-1].A)
-    except RuntimeError as exc:
-        raise RuntimeError(str(exc)) from exc
+        sym = _is_symmetric(A_p)
+        while True:
+            if A_l.nrows <= params.coarsest_size or len(pending) + 1 >= params.max_levels:
+                break
+            agg = pairwise_aggregate(A_l, params.theta_amg)
+            if agg.n_aggregates > 0.9 * A_l.nrows:
+                break
+            pending.append((len(pending), A_l, agg, pool.submit(_smooth_level, A_l, params)))
+            A_l = _galerkin(A_l, agg)
+        inv = _dense_inverse(A_l)
+    except Exception as exc:
+        earlier = first_smoother_error()
+        if earlier is not None:
+            raise earlier from None
+        if isinstance(exc, RuntimeError):
+            raise RuntimeError(str(exc)) from exc
+        raise
+    for _, A_s, agg, fut in pending:
+        partition, smoother = fut.result()
+        levels.append(AmgLevel(A_s, partition, smoother, P=_prolongation(agg, A_s.nrows),
+                               aggregates=agg.aggregate_of))
+    levels.append(AmgLevel(A_l, None, None))
     return AmgHierarchy(levels, ("inverse", inv), params, symmetric=sym)
 
 
@@ -252,10 +292,43 @@ def _permuted_rows_sell(A, perm: np.ndarray, inv: np.ndarray):
     return D.pack_sell(lane_row, lane_ptr, cols, vals, 1, n)
 
 
-LV1_ROWS = 0  # coarse levels at most this large run each V-cycle pass in ONE CTA (csrc/amg.cu k_lv_fwd/k_lv_bwd)
-TAIL_ROWS = 0  # levels at most this large run in the persistent tail kernel (0 = off)
-TAIL3_CTAS = 16          # cluster size of the smem-resident tail
-TAIL3_SMEM_MAX = 200 * 1024  # per-CTA packed bytes (dynamic shared memory)
+# persistent single-CTA V-cycle tail (csrc/vtail.cu): the coarse levels whose
+# vectors fit TAIL_VEC_BYTES of shared memory run in one launch
+# (CPRB_TAIL_ROWS = largest level admitted; 0 = off)
+TAIL_ROWS = 0  # off until the tail beats the launched chain (set after measuring)
+TAIL_VEC_BYTES = int(os.environ.get("CPRB_TAIL_VEC_KB", "150")) * 1024
+TAIL_SMEM = 227 * 1024
+TAIL_NSLOT = 4
+VT_SWEEP, VT_RR, VT_COARSE, VT_PROLONG = 1, 3, 4, 5
+
+
+class _ChunkStream:
+    """Phase-ordered stream of <= slot-byte records (16-byte aligned
+    sections) for the tail's TMA producer."""
+
+    def __init__(self, slot):
+        self.slot = slot
+        self.parts, self.chunks, self.phases = [], [], []
+        self.off = 0
+
+    def phase(self, typ, level, colour):
+        self.phases.append((typ, level, colour, len(self.chunks)))
+
+    def chunk(self, rows, *arrays):
+        raw = bytearray()
+        for a in arrays:
+            b = np.ascontiguousarray(a).tobytes()
+            raw.extend(b)
+            raw.extend(b"\0" * ((-len(b)) % 16))
+        if len(raw) > self.slot:
+            raise ValueError("tail chunk exceeds its ring slot")
+        self.chunks.append((len(self.phases) - 1, self.off // 16, len(raw), rows))
+        self.parts.append(bytes(raw))
+        self.off += len(raw)
+
+    def rows_per_chunk(self, per_row, fixed=16, multiple=1):
+        r = max(1, (self.slot - fixed - 64) // max(per_row, 1))
+        return max(multiple, (r // multiple) * multiple)
 
 
 class DeviceAmg:
@@ -284,21 +357,29 @@ class DeviceAmg:
         self.levels = []
         self.restrict = []
         self.aggp = []
+        self.aggp_host = []
         self.kspmv = []
-        for l in range(L - 1):
-            lvl = h.levels[l]
+        for lvl in h.levels[:-1]:
             if not isinstance(lvl.smoother, PgsScmSmoother):
                 raise NotImplementedError("device AMG levels use the PGS-SCM smoother")
+
+        def pack(l):
+            # one level's device layouts (independent of every other level)
+            lvl = h.levels[l]
             dl = lvl.smoother.device()
             na = h.levels[l + 1].A.nrows
             R = D.SellDev(_restriction_sell(lvl.A, lvl.aggregates, na, invs[l], invs[l + 1]))
-            aggp = D.upload(invs[l + 1][lvl.aggregates[perms[l]]].astype(np.int32))
+            aggp_h = invs[l + 1][lvl.aggregates[perms[l]]].astype(np.int32)
+            return dl, R, D.upload(aggp_h), aggp_h
+
+        packed = list(setup_pool().map(D.bind_current(pack), range(L - 1)))
+        for l in range(L - 1):
+            lvl = h.levels[l]
+            dl, R, aggp, aggp_h = packed[l]
+            self.aggp_host.append(aggp_h)
             dl.desc.restrict_op = R.desc
             dl.desc.restrict_width = int(R.host.lane_len.max()) if R.host.lane_len.size else 0
             dl.desc.aggp = D.ptr(aggp)
-            lim = int(os.environ.get("CPRB_LV1_ROWS", str(LV1_ROWS)))
-            dl.desc.one_cta = 1 if (l >= 1 and lvl.A.nrows <= lim and dl.desc.ncolors > 1
-                                    and not dl.snapshot.any()) else 0
             self.levels.append(dl)
             self.restrict.append(R)
             self.aggp.append(aggp)
@@ -327,154 +408,142 @@ class DeviceAmg:
         self._build_tail()
 
     def _build_tail(self):
-        """Phase table and packed per-CTA static data of the levels handled by
-        the persistent cluster tail kernel (csrc/amg.cu k_vtail3): every level
-        with at most TAIL_ROWS rows (CPRB_TAIL_ROWS overrides; 0 = off)."""
+        """Stream of the persistent V-cycle tail (csrc/vtail.cu): the deepest
+        run of levels (>= 1) whose b and x fit TAIL_VEC_BYTES of shared
+        memory, each with several colours and no intra-colour couplings
+        (those levels keep the launched path), plus the coarse solve.  The
+        records restate exactly the launched kernels' inputs: sweep rows
+        (permuted, ascending permuted columns, the zero-guess prefix length
+        on the way down), restriction lane pairs (original column order),
+        aggregate maps and coarse-inverse rows."""
         L = self.nlevels
         self.desc.tail_start = L - 1
-        self.desc.tail_mode = 0
-        if L <= 1:
+        if L <= 2:
             return
         limit = int(os.environ.get("CPRB_TAIL_ROWS", str(TAIL_ROWS)))
+        nc = self.n_coarse
         ts = L - 1
-        for l in range(1, L - 1):
-            if self.h.levels[l].A.nrows <= limit:
-                ts = l
+        vec_bytes = 16 * nc
+        for l in range(L - 2, 0, -1):
+            dl = self.levels[l]
+            n = int(dl.desc.n)
+            if (n > limit or n >= 65536 or dl.desc.ncolors < 2 or dl.snapshot.any()
+                    or vec_bytes + 16 * n > TAIL_VEC_BYTES):
                 break
+            vec_bytes += 16 * n
+            ts = l
         if ts >= L - 1:
             return
-        arr = (N.TailLevel * (L - 1))()
-        for l, dl in enumerate(self.levels):
-            d = dl.desc
-            t = arr[l]
-            t.smoother = d.smoother
-            t.restrict_op = d.restrict_op
-            t.diag, t.aggp, t.b, t.x, t.tmp = d.diag, d.aggp, d.b, d.x, d.tmp
-            t.n, t.ncolors, t.color_off = d.n, d.ncolors, 0
-        # phase table {type, level, colour, flags} (csrc/amg.cu TP_*): flags
-        # bit0 = zero-guess prefix (forward), 0 = full row (backward)
-        SWEEP, RR, COARSE, PROLONG = 1, 3, 4, 5
-        ph = []
-        for l in range(ts, L - 1):
-            dl = self.levels[l]
-            if dl.desc.ncolors == 1 or dl.snapshot.any():
-                return                  # sequential GS / snapshot colours: launch path
-            ph += [(SWEEP, l, k, 1) for k in range(dl.desc.ncolors)]
-            ph.append((RR, l, 0, 0))
-        ph.append((COARSE, 0, 0, 0))
-        for l in range(L - 2, ts - 1, -1):
-            ph.append((PROLONG, l, 0, 0))
-            ph += [(SWEEP, l, k, 0) for k in range(self.levels[l].desc.ncolors - 1, -1, -1)]
-        self.tail_phase_list = ph
-        packed = self._build_tail3(ts, nctas=TAIL3_CTAS)
-        if packed is None:
+        vec = np.full(2 * L, -1, dtype=np.int32)
+        off = 0
+        for l in list(range(ts, L - 1)) + [L - 1]:
+            n = nc if l == L - 1 else int(self.levels[l].desc.n)
+            vec[2 * l], vec[2 * l + 1] = off, off + n
+            off += 2 * n
+        vec_len = off
+        vbytes = (vec_len * 8 + 127) & ~127
+        nph = 1 + sum(2 * int(self.levels[l].desc.ncolors) + 2 for l in range(ts, L - 1))
+        meta = 64 + 16 * (nph + 1) + 8 * L + 128      # mbarriers, phase table, offsets
+        slot = min(32 * 1024, ((TAIL_SMEM - vbytes - meta) // TAIL_NSLOT) // 16 * 16)
+        if slot < max(4096, 8 * nc + 64):
             return
-        flat, seg, maxb = packed
-        self.tail_levels = D.upload(np.frombuffer(bytes(arr), dtype=np.uint8).copy())
-        self.tail_phases = D.upload(np.asarray(ph, dtype=np.int32).reshape(-1))
-        self.tail3_buf = D.upload(flat)
-        self.tail3_seg = D.upload(seg.reshape(-1))
-        self.desc.tail_levels = D.ptr(self.tail_levels)
-        self.desc.tail_phases = D.ptr(self.tail_phases)
-        self.desc.tail_nphases = len(ph)
-        self.desc.tail3_buf = D.ptr(self.tail3_buf)
-        self.desc.tail3_seg = D.ptr(self.tail3_seg)
-        self.desc.tail3_max_bytes = int(maxb)
-        self.desc.tail_ctas = TAIL3_CTAS
-        self.desc.tail_start = ts
-        self.desc.tail_mode = 3
+        st = _ChunkStream(slot)
+        for l in range(ts, L - 1):
+            sp = self.h.levels[l].smoother.split
+            for k in range(sp.ncolors):
+                self._tail_sweep(st, l, sp, k, True)
+            self._tail_rr(st, l)
+        inv = np.ascontiguousarray(self.h.coarsest_lu[1], dtype=np.float64)
+        st.phase(VT_COARSE, L - 1, 0)
+        per = st.rows_per_chunk(8 * nc)
+        for a in range(0, nc, per):
+            e = min(nc, a + per)
+            st.chunk(e - a, np.array([e - a, nc, a, 0], dtype=np.int32), inv[a:e])
+        for l in range(L - 2, ts - 1, -1):
+            aggp = self.aggp_host[l]
+            st.phase(VT_PROLONG, l, 0)
+            n = aggp.shape[0]
+            per = st.rows_per_chunk(4)
+            for a in range(0, n, per):
+                e = min(n, a + per)
+                st.chunk(e - a, np.array([e - a, 0, a, 0], dtype=np.int32), aggp[a:e])
+            sp = self.h.levels[l].smoother.split
+            for k in range(sp.ncolors - 1, -1, -1):
+                self._tail_sweep(st, l, sp, k, False)
+        phases = np.asarray(st.phases + [(0, 0, 0, len(st.chunks))], dtype=np.int32)
+        self.tail_phase_host = [p + (sum(1 for c in st.chunks if c[0] == i),)
+                                for i, p in enumerate(st.phases)]
+        self.tail_phases = D.upload(phases.reshape(-1))
+        self.tail_chunks = D.upload(np.asarray(st.chunks, dtype=np.int32).reshape(-1))
+        self.tail_stream = D.upload(np.frombuffer(b"".join(st.parts), dtype=np.uint8).copy())
+        self.tail_vec = D.upload(vec)
+        d = self.desc
+        d.tail_nphases = len(st.phases)
+        d.tail_nchunks = len(st.chunks)
+        d.tail_slot = slot
+        d.tail_vec_len = vec_len
+        d.tail_smem = vbytes + TAIL_NSLOT * slot + meta
+        d.tail_phases = D.ptr(self.tail_phases)
+        d.tail_chunks = D.ptr(self.tail_chunks)
+        d.tail_stream = D.ptr(self.tail_stream)
+        d.tail_vec = D.ptr(self.tail_vec)
+        d.tail_stream_bytes = st.off
+        d.tail_start = ts
+        self.tail_bytes = st.off
 
-    # -- smem-resident cluster tail (csrc/amg.cu k_vtail3) ------------------------
-    def _build_tail3(self, ts: int, nctas: int = 16):
-        """Pack the static data of levels >= ts (colour sweeps, residual +
-        restriction, prolongation maps, coarse inverse rows) into one byte
-        buffer per CTA of a `nctas` cluster, one 16-byte aligned segment per
-        phase of self.tail_phase_list.  Returns None if the largest CTA
-        buffer exceeds shared memory."""
-        ph = np.asarray(self.tail_phase_list, dtype=np.int32)
-        SWEEP, RR, COARSE, PROLONG = 1, 3, 4, 5
-        if ts == 0:
-            return None
-        bufs = [bytearray() for _ in range(nctas)]
-        seg = np.zeros((nctas, len(ph) + 1), dtype=np.int64)
+    @staticmethod
+    def _tail_sweep(st, l, sp, k, zg):
+        r0, r1 = int(sp.color_rows[k]), int(sp.color_rows[k + 1])
+        st.phase(VT_SWEEP, l, k | (0x100 if zg else 0))
+        rows = np.arange(r0, r1, dtype=np.int64)
+        lo, hi = sp.off_ptr[rows], sp.off_ptr[rows + 1]
+        if zg:   # zero guess: only the entries whose columns precede the colour
+            lens = np.array([int(np.searchsorted(sp.off_cols[x:y], r0)) for x, y in zip(lo, hi)],
+                            dtype=np.int64)
+        else:
+            lens = hi - lo
+        Wp = int(lens.max()) if lens.size else 0
+        per = st.rows_per_chunk(12 + 10 * Wp, fixed=48)
+        for a in range(0, r1 - r0, per):
+            e = min(r1 - r0, a + per)
+            cnt = e - a
+            ln = lens[a:e]
+            W = int(ln.max()) if cnt else 0
+            cols = np.zeros((W, cnt), dtype=np.uint16)
+            vals = np.zeros((W, cnt), dtype=np.float64)
+            for t in range(cnt):
+                m = int(ln[t])
+                x = int(lo[a + t])
+                cols[:m, t] = sp.off_cols[x:x + m]
+                vals[:m, t] = sp.off_vals[x:x + m]
+            st.chunk(cnt, np.array([cnt, W, r0 + a, int(zg)], dtype=np.int32),
+                     ln.astype(np.int32), sp.diag[r0 + a:r0 + e].astype(np.float64), cols, vals)
 
-        def put(q, *arrays):
-            b = bufs[q]
-            for a in arrays:
-                raw = np.ascontiguousarray(a).tobytes()
-                b.extend(raw)
-                b.extend(b"\0" * ((-len(raw)) % 16))
-
-        def split(n):
-            m = -(-n // nctas)
-            return [(min(q * m, n), min((q + 1) * m, n)) for q in range(nctas)]
-
-        inv = self.h.coarsest_lu[1]
-        for pi, (typ, l, k, flags) in enumerate(ph):
-            for q in range(nctas):
-                seg[q, pi] = len(bufs[q])
-            if typ == SWEEP:
-                sp = self.h.levels[l].smoother.split
-                r0, r1 = int(sp.color_rows[k]), int(sp.color_rows[k + 1])
-                for q, (a, e) in enumerate(split(r1 - r0)):
-                    rows = np.arange(r0 + a, r0 + e, dtype=np.int64)
-                    cnt = rows.shape[0]
-                    lo, hi = sp.off_ptr[rows], sp.off_ptr[rows + 1]
-                    lens = hi - lo
-                    if flags & 1:   # zero-guess prefix: columns before the colour
-                        lens = np.array([int(np.searchsorted(sp.off_cols[x:y], r0)) for x, y in
-                                         zip(lo, hi)], dtype=np.int64) if cnt else lens
-                    W = int(lens.max()) if cnt else 0
-                    cols = np.zeros((W, cnt), dtype=np.int32)
-                    vals = np.zeros((W, cnt), dtype=np.float64)
-                    for t in range(cnt):
-                        L_ = int(lens[t])
-                        cols[:L_, t] = sp.off_cols[lo[t]:lo[t] + L_]
-                        vals[:L_, t] = sp.off_vals[lo[t]:lo[t] + L_]
-                    put(q, np.array([cnt, W, r0 + a, 0], dtype=np.int32), lens.astype(np.int32),
-                        sp.diag[rows].astype(np.float64), cols, vals)
-            elif typ == RR:
-                R = self.restrict[l].host
-                na = self.h.levels[l + 1].A.nrows
-                lr = R.lane_row.astype(np.int64)
-                for q, (a, e) in enumerate(split(na)):
-                    lanes = np.arange(2 * a, 2 * e, dtype=np.int64)
-                    cnt = lanes.shape[0]
-                    rows = lr[lanes]
-                    lens = np.where(rows >= 0, R.lane_len[lanes], 0).astype(np.int64)
-                    W = int(lens.max()) if cnt else 0
-                    cols = np.zeros((W, cnt), dtype=np.int32)
-                    vals = np.zeros((W, cnt), dtype=np.float64)
-                    sl, ln = lanes // 32, lanes % 32
-                    for m in range(W):
-                        ok = m < lens
-                        ent = R.slice_ptr[sl[ok]] + 32 * m + ln[ok]
-                        cols[m, ok] = R.cols[ent]
-                        vals[m, ok] = R.vals[ent]
-                    out = R.agg_out[np.arange(a, e)].astype(np.int32)
-                    put(q, np.array([cnt, W, 0, 0], dtype=np.int32), rows.astype(np.int32),
-                        lens.astype(np.int32), out, cols, vals)
-            elif typ == PROLONG:
-                aggp = self.aggp[l].cpu().numpy()
-                n = aggp.shape[0]
-                for q, (a, e) in enumerate(split(n)):
-                    put(q, np.array([e - a, 0, a, 0], dtype=np.int32), aggp[a:e])
-            elif typ == COARSE:
-                n = inv.shape[0]
-                for q, (a, e) in enumerate(split(n)):
-                    put(q, np.array([e - a, n, a, 0], dtype=np.int32),
-                        np.ascontiguousarray(inv[a:e], dtype=np.float64))
-        for q in range(nctas):
-            seg[q, len(ph)] = len(bufs[q])
-        maxb = max(len(b) for b in bufs)
-        self.tail3_bytes = maxb
-        if maxb > TAIL3_SMEM_MAX:
-            return None
-        base = np.zeros(nctas + 1, dtype=np.int64)
-        np.cumsum([len(b) for b in bufs], out=base[1:])
-        flat = np.frombuffer(b"".join(bytes(b) for b in bufs), dtype=np.uint8).copy()
-        seg = seg + base[:-1, None]          # absolute byte offsets into the flat buffer
-        return flat, seg, maxb
+    def _tail_rr(self, st, l):
+        R = self.restrict[l].host
+        st.phase(VT_RR, l, 0)
+        lr = R.lane_row.astype(np.int64)
+        nl_ = lr.shape[0]
+        lens_all = np.where(lr >= 0, R.lane_len, 0).astype(np.int64)
+        Wp = int(lens_all.max()) if nl_ else 0
+        per = st.rows_per_chunk(10 + 10 * Wp, fixed=64, multiple=32)
+        for a in range(0, nl_, per):
+            e = min(nl_, a + per)
+            lanes = np.arange(a, e, dtype=np.int64)
+            cnt = e - a
+            ln = lens_all[a:e]
+            W = int(ln.max()) if cnt else 0
+            cols = np.zeros((W, cnt), dtype=np.uint16)
+            vals = np.zeros((W, cnt), dtype=np.float64)
+            sl, lane = lanes // 32, lanes % 32
+            for m in range(W):
+                ok = m < ln
+                ent = R.slice_ptr[sl[ok]] + 32 * m + lane[ok]
+                cols[m, ok] = R.cols[ent]
+                vals[m, ok] = R.vals[ent]
+            outs = R.agg_out[a // 2:e // 2].astype(np.int32)
+            st.chunk(cnt, np.array([cnt, W, 0, 0], dtype=np.int32), lr[a:e].astype(np.int32),
+                     ln.astype(np.int32), outs, cols, vals)
 
     # -- V-cycle: one native call ------------------------------------------------
     def vcycle(self, r, z):

@@ -12,6 +12,7 @@
 
 #include "device.cuh"
 #include "engine.h"
+#include "nvtx.h"
 
 namespace cprb {
 
@@ -391,217 +392,6 @@ __global__ void k_scatter(int n, const int32_t* __restrict__ idx, const double* 
   if (i < n) dst[idx ? idx[i] : i] = src[i];
 }
 
-// ---------------------------------------------------------------------------
-// Persistent V-cycle tail (k_vtail3 below).  Levels >= tail_start (their
-// colour sweeps, fused residual + restriction, prolongation) and the coarse
-// solve run in ONE kernel launched as a single 16-CTA thread-block cluster,
-// driven by a phase table {type, level, colour, flags} built by
-// amg.DeviceAmg._build_tail.
-// ---------------------------------------------------------------------------
-enum { TP_SWEEP = 1, TP_RR = 3, TP_COARSE = 4, TP_PROLONG = 5 };
-
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-
-// ---------------------------------------------------------------------------
-// Shared-memory-resident cluster tail (k_vtail3).  Every CTA of a 16-CTA
-// cluster loads, once per launch, its slice of the static data of every
-// phase (packed by amg.DeviceAmg._build_tail3: row lengths, diagonal,
-// columns and values of its rows of each colour sweep, its aggregates of
-// each restriction, its prolongation map entries and coarse-inverse rows)
-// into shared memory.  A phase is then: all x gathers of a row in flight at
-// once (L2), arithmetic, one store, one cluster barrier.  Same arithmetic
-// order as the per-colour kernels (bit-identical).
-// ---------------------------------------------------------------------------
-constexpr int TAIL3_THREADS = 512;
-
-struct Tail3Args {
-  const cprb_tail_level* lev;
-  const int4* phases;
-  int nphases;
-  int nl;
-  double* coarse_b;
-  double* coarse_x;
-  const uint8_t* buf;
-  const int64_t* seg;  // [ctas][nphases + 1]
-};
-
-__device__ __forceinline__ void cluster_sync_all() {
-  __syncwarp();
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-
-__device__ __forceinline__ const uint8_t* align16(const uint8_t* p) {
-  return reinterpret_cast<const uint8_t*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
-}
-
-__device__ unsigned long long* g_tail3_log = nullptr;  // diagnostic: per-phase end times (CTA 0)
-
-__global__ void __launch_bounds__(TAIL3_THREADS, 1) k_vtail3(const Tail3Args a) {
-  extern __shared__ __align__(16) uint8_t sm3[];
-  __shared__ double* s_x[32];  // per-level vector pointers (no global struct reloads
-  __shared__ double* s_b[32];  // after every cluster barrier)
-  unsigned long long* const tl = g_tail3_log;
-  if (tl && blockIdx.x == 0 && threadIdx.x == 0) tl[0] = gtimer();
-  const int q = blockIdx.x;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  constexpr int NW = TAIL3_THREADS / 32;
-  if (tid < a.nl - 1 && tid < 32) {
-    s_x[tid] = a.lev[tid].x;
-    s_b[tid] = a.lev[tid].b;
-  }
-  const int64_t* segq = a.seg + (int64_t)q * (a.nphases + 1);
-  const int64_t base = segq[0];
-  const int64_t nbytes = segq[a.nphases] - base;
-  {  // one-time load of this CTA's static data (16-byte vectors)
-    const int4* src = reinterpret_cast<const int4*>(a.buf + base);
-    int4* dst = reinterpret_cast<int4*>(sm3);
-    for (int64_t i = tid; i < nbytes / 16; i += TAIL3_THREADS) dst[i] = __ldg(src + i);
-  }
-  __syncthreads();
-  cluster_sync_all();
-  for (int p = 0; p < a.nphases; ++p) {
-    const int4 ph = __ldg(a.phases + p);
-    const uint8_t* s = sm3 + (segq[p] - base);
-    const int* hdr = reinterpret_cast<const int*>(s);
-    const int cnt = hdr[0], W = hdr[1], first = hdr[2];
-    const uint8_t* body = s + 16;
-    switch (ph.x) {
-      case TP_SWEEP: {
-        double* const Lx = s_x[ph.y];
-        const double* const Lb = s_b[ph.y];
-        const int* lens = reinterpret_cast<const int*>(body);
-        const double* diag = reinterpret_cast<const double*>(align16(body + 4 * cnt));
-        const int* cols = reinterpret_cast<const int*>(align16(reinterpret_cast<const uint8_t*>(diag + cnt)));
-        const double* vals = reinterpret_cast<const double*>(align16(reinterpret_cast<const uint8_t*>(cols + (size_t)W * cnt)));
-        for (int t = tid; t < cnt; t += TAIL3_THREADS) {
-          const int len = lens[t];
-          const int row = first + t;
-          const double bi = __ldcg(Lb + row);
-          double acc = 0.0;
-          if (len <= 32) {  // every gather of the row in flight at once
-            double xv[32];
-#pragma unroll
-            for (int u = 0; u < 32; ++u) xv[u] = (u < len) ? __ldcg(Lx + cols[(size_t)u * cnt + t]) : 0.0;
-#pragma unroll
-            for (int u = 0; u < 32; ++u)
-              if (u < len) acc = acc + vals[(size_t)u * cnt + t] * xv[u];
-          } else {
-            for (int m = 0; m < len; ++m) acc = acc + vals[(size_t)m * cnt + t] * __ldcg(Lx + cols[(size_t)m * cnt + t]);
-          }
-          Lx[row] = (bi - acc) / diag[t];
-        }
-        break;
-      }
-      case TP_RR: {
-        const double* const Lx = s_x[ph.y];
-        const double* const Lb = s_b[ph.y];
-        double* bc = (ph.y + 1 < a.nl - 1) ? s_b[ph.y + 1] : a.coarse_b;
-        const int* rows = reinterpret_cast<const int*>(body);
-        const int* lens = reinterpret_cast<const int*>(align16(body + 4 * cnt));
-        const int* outs = reinterpret_cast<const int*>(align16(reinterpret_cast<const uint8_t*>(lens + cnt)));
-        const int* cols = reinterpret_cast<const int*>(align16(reinterpret_cast<const uint8_t*>(outs + cnt / 2)));
-        const double* vals = reinterpret_cast<const double*>(align16(reinterpret_cast<const uint8_t*>(cols + (size_t)W * cnt)));
-        // lanes 2I, 2I+1 of an aggregate are adjacent threads of one warp
-        for (int t0 = 0; t0 < cnt; t0 += TAIL3_THREADS) {
-          const int t = t0 + tid;
-          double res = 0.0;
-          if (t < cnt) {
-            const int row = rows[t];
-            const int len = lens[t];
-            if (row >= 0) {
-              double tsum;
-              if (len <= 32) {
-                double e[32];
-#pragma unroll
-                for (int mm = 0; mm < 32; ++mm)
-                  e[mm] = (mm < len) ? vals[(size_t)mm * cnt + t] * __ldcg(Lx + cols[(size_t)mm * cnt + t]) : 0.0;
-                tsum = segsum_masked<32>(e, len);
-              } else {
-                auto f = [&](int mm) -> double {
-                  return vals[(size_t)mm * cnt + t] * __ldcg(Lx + cols[(size_t)mm * cnt + t]);
-                };
-                tsum = segsum_rt(f, len);
-              }
-              res = __ldcg(Lb + row) - tsum;
-            }
-          }
-          const double other = __shfl_down_sync(CPRB_FULL, res, 1);
-          if (t < cnt && (t & 1) == 0) {
-            const int out = outs[t >> 1];
-            if (out >= 0) bc[out] = (0.0 + res) + other;
-          }
-        }
-        break;
-      }
-      case TP_PROLONG: {
-        double* const Lx = s_x[ph.y];
-        const double* xc = (ph.y + 1 < a.nl - 1) ? s_x[ph.y + 1] : a.coarse_x;
-        const int* aggp = reinterpret_cast<const int*>(body);
-        for (int t = tid; t < cnt; t += TAIL3_THREADS) {
-          const int i = first + t;
-          Lx[i] = __ldcg(Lx + i) + __ldcg(xc + aggp[t]);
-        }
-        break;
-      }
-      case TP_COARSE: {
-        const double* rowsd = reinterpret_cast<const double*>(body);
-        for (int r = wid; r < cnt; r += NW) {
-          const double* row = rowsd + (size_t)r * W;
-          double sacc = 0.0;
-          for (int c = lane; c < W; c += 32) sacc = sacc + row[c] * __ldcg(a.coarse_b + c);
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) sacc = sacc + __shfl_xor_sync(CPRB_FULL, sacc, o);
-          if (lane == 0) a.coarse_x[first + r] = sacc;
-        }
-        break;
-      }
-      default:
-        break;
-    }
-    cluster_sync_all();
-    if (tl && blockIdx.x == 0 && threadIdx.x == 0) tl[1 + p] = gtimer();
-  }
-}
-
-static int launch_vtail3(const cprb_amg& h, cudaStream_t st) {
-  static bool attr = false;
-  const int g = h.tail_ctas > 0 ? h.tail_ctas : 16;
-  if (!attr) {
-    cudaFuncSetAttribute(k_vtail3, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(k_vtail3, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
-  Tail3Args ta;
-  ta.lev = h.tail_levels;
-  ta.phases = reinterpret_cast<const int4*>(h.tail_phases);
-  ta.nphases = h.tail_nphases;
-  ta.nl = h.nlevels;
-  ta.coarse_b = h.coarse_b;
-  ta.coarse_x = h.coarse_x;
-  ta.buf = h.tail3_buf;
-  ta.seg = h.tail3_seg;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(g);
-  cfg.blockDim = dim3(TAIL3_THREADS);
-  cfg.dynamicSmemBytes = (size_t)((h.tail3_max_bytes + 15) & ~15);
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = g;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k_vtail3, ta);
-  if (e != cudaSuccess)
-    return set_error(CPRB_EDEVICE, std::string("v-cycle smem tail launch: ") + cudaGetErrorString(e));
-  return check_launch("v-cycle smem tail");
-}
-
 template <int ZG, int G, int SC>
 static void launch_sweep(const cprb_amg_level& L, int k, double* b, const double* gsrc,
                          int gstride, const int32_t* perm, const double* xin, double* xout,
@@ -656,241 +446,8 @@ int pgs_pass(const cprb_amg_level& L, const double* b_in, double* x, int dir, in
   return check_launch("pgs pass");
 }
 
-// ---------------------------------------------------------------------------
-// Single-CTA level passes (coarse levels of the V-cycle).  A coarse level's
-// colour sweeps cost one dependent launch each (~3 us) while its work is a
-// few microseconds, so a level with at most a few thousand rows runs its
-// whole forward pass (zero-guess colour sweeps + fused residual/restriction)
-// in ONE CTA and its whole backward pass (prolongation + reverse colour
-// sweeps) in another: x lives in shared memory, colours are separated by
-// __syncthreads, and every row is summed exactly as k_sweep /
-// k_resid_restrict sum it (bitwise identical results).
-constexpr int LV_THREADS = 256;
-constexpr int LV_MAXC = 32;
-
-struct LvArgs {
-  cprb_sell S;  // smoother (off-diagonals, colour slices)
-  cprb_sell R;  // restriction (aggregate lane pairs, original column order)
-  const double* diag;
-  const int32_t* aggp;
-  const double* b;
-  double* x;
-  int n, nc, fused;
-  int cs[LV_MAXC + 1];
-  int cr[LV_MAXC + 1];
-  double* bc;         // forward: next level's b (or the coarse b)
-  double* xn;         // forward: next level's x (fused first colour) or nullptr
-  const double* dn;
-  int c0n;
-  const double* xc;   // backward: coarse correction
-};
-
-// reduceat row sum a0 + pairwise8(rest) over a generic x (shared memory)
-__device__ __forceinline__ double rr_row_gen(const cprb_sell& R, int64_t base, int len,
-                                             const double* x) {
-  if (len > 129) {
-    auto f = [&](int m) -> double {
-      const int64_t e = base + (int64_t)m * 32;
-      return __ldg(R.vals + e) * x[__ldg(R.cols + e)];
-    };
-    return segsum_rt(f, len);
-  }
-  if (len <= 0) return 0.0;
-  const int nr = len - 1;
-  const int nf = nr >= 8 ? (nr & ~7) : 0;
-  double a0 = 0.0, s = -0.0, r8[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) r8[k] = 0.0;
-  for (int p = 0; p < len; ++p) {
-    const int64_t e = base + (int64_t)p * 32;
-    const double v = __ldg(R.vals + e) * x[__ldg(R.cols + e)];
-    if (p == 0) {
-      a0 = v;
-      continue;
-    }
-    const int q = p - 1;
-    if (q < nf) {
-      if (q < 8) r8[q & 7] = v;
-      else r8[q & 7] = r8[q & 7] + v;
-      if (q == nf - 1) s = ((r8[0] + r8[1]) + (r8[2] + r8[3])) + ((r8[4] + r8[5]) + (r8[6] + r8[7]));
-    } else {
-      s = s + v;
-    }
-  }
-  return a0 + s;
-}
-
-// one row of a colour: static data prefetched into registers (a colour's
-// rows are loaded while the previous colour is being computed)
-constexpr int LV_CH = 16;
-struct LvRow {
-  int row, len;
-  int64_t base;
-  double d, bi;
-  int c[LV_CH];
-  double v[LV_CH];
-};
-
-template <int ZG>
-__device__ __forceinline__ LvRow lv_load(const LvArgs& a, int k, int r) {
-  LvRow q;
-  q.row = -1;
-  q.len = 0;
-  if (k < 0 || k >= a.nc) return q;
-  const int r0 = a.cr[k];
-  if (r >= a.cr[k + 1] - r0) return q;
-  const int w = a.cs[k] + (r >> 5), lane = r & 31;
-  const int lid = w * 32 + lane;
-  q.len = ZG ? __ldg(a.S.lane_len_lo + lid) : __ldg(a.S.lane_len + lid);
-  q.base = __ldg(a.S.slice_ptr + w) + lane;
-  q.row = r0 + r;
-  q.d = __ldg(a.diag + q.row);
-  q.bi = __ldcg(a.b + q.row);
-#pragma unroll
-  for (int m = 0; m < LV_CH; ++m)
-    if (m < q.len) {
-      q.c[m] = __ldg(a.S.cols + q.base + (int64_t)m * 32);
-      q.v[m] = __ldg(a.S.vals + q.base + (int64_t)m * 32);
-    }
-  return q;
-}
-
-__device__ __forceinline__ void lv_row(const LvArgs& a, const LvRow& q, double* sx) {
-  if (q.row < 0) return;
-  double acc = 0.0;
-#pragma unroll
-  for (int m = 0; m < LV_CH; ++m)
-    if (m < q.len) acc = acc + q.v[m] * sx[q.c[m]];
-  for (int m = LV_CH; m < q.len; ++m) {
-    const int64_t e = q.base + (int64_t)m * 32;
-    acc = acc + __ldg(a.S.vals + e) * sx[__ldg(a.S.cols + e)];
-  }
-  sx[q.row] = (q.bi - acc) / q.d;
-}
-
-// colours kbeg, kbeg+dk, ... (nk of them); the first row of every thread in
-// the next colour is prefetched before this colour's barrier
-template <int ZG>
-__device__ __forceinline__ void lv_pass(const LvArgs& a, int kbeg, int dk, int nk, double* sx) {
-  LvRow cur = lv_load<ZG>(a, kbeg, threadIdx.x);
-  for (int t = 0; t < nk; ++t) {
-    const int k = kbeg + t * dk;
-    const LvRow nxt = lv_load<ZG>(a, t + 1 < nk ? k + dk : -1, threadIdx.x);
-    lv_row(a, cur, sx);
-    const int nr = a.cr[k + 1] - a.cr[k];
-    for (int r = threadIdx.x + LV_THREADS; r < nr; r += LV_THREADS) lv_row(a, lv_load<ZG>(a, k, r), sx);
-    __syncthreads();
-    cur = nxt;
-  }
-}
-
-__global__ void __launch_bounds__(LV_THREADS, 1) k_lv_fwd(const LvArgs a) {
-  extern __shared__ double sx[];
-  pdl_trigger();
-  AmgMark mk;
-  mk.start(6);
-  pdl_wait();
-  mk.waited();
-  int k0 = 0;
-  if (a.fused) {  // colour 0 already computed by the previous restriction
-    for (int i = threadIdx.x; i < a.cr[1]; i += LV_THREADS) sx[i] = __ldcg(a.x + i);
-    k0 = 1;
-  }
-  __syncthreads();
-  lv_pass<1>(a, k0, 1, a.nc - k0, sx);
-  for (int i = threadIdx.x; i < a.n; i += LV_THREADS) a.x[i] = sx[i];
-  // fused residual + restriction (k_resid_restrict), x from shared memory:
-  // a row's entries are loaded in one batch, then summed in reduceat order
-  const int lane = threadIdx.x & 31;
-  for (int w = threadIdx.x >> 5; w < a.R.nslices; w += LV_THREADS / 32) {
-    const int lid = w * 32 + lane;
-    const int row = __ldg(a.R.lane_row + lid);
-    const int len = row >= 0 ? __ldg(a.R.lane_len + lid) : 0;
-    const int64_t base = __ldg(a.R.slice_ptr + w) + lane;
-    const int out = ((lane & 1) == 0) ? __ldg(a.R.agg_out + w * 16 + (lane >> 1)) : -1;
-    constexpr int P = 32;
-    int c[P];
-    double e[P];
-#pragma unroll
-    for (int m = 0; m < P; ++m)
-      if (m < len) {
-        c[m] = __ldg(a.R.cols + base + (int64_t)m * 32);
-        e[m] = __ldg(a.R.vals + base + (int64_t)m * 32);
-      }
-    double res = 0.0;
-    if (row >= 0) {
-      const double bi = __ldcg(a.b + row);
-      double t;
-      if (len <= P) {
-#pragma unroll
-        for (int m = 0; m < P; ++m) e[m] = (m < len) ? e[m] * sx[c[m]] : 0.0;
-        t = segsum_masked<P>(e, len);
-      } else {
-        t = rr_row_gen(a.R, base, len, sx);
-      }
-      res = bi - t;
-    }
-    const double other = __shfl_down_sync(CPRB_FULL, res, 1);
-    if ((lane & 1) == 0 && out >= 0) {
-      const double bcv = (0.0 + res) + other;
-      a.bc[out] = bcv;
-      if (a.xn && out < a.c0n) a.xn[out] = (bcv - 0.0) / a.dn[out];
-    }
-  }
-  mk.end();
-}
-
-__global__ void __launch_bounds__(LV_THREADS, 1) k_lv_bwd(const LvArgs a) {
-  extern __shared__ double sx[];
-  pdl_trigger();
-  AmgMark mk;
-  mk.start(7);
-  pdl_wait();
-  mk.waited();
-  for (int i = threadIdx.x; i < a.n; i += LV_THREADS)
-    sx[i] = __ldcg(a.x + i) + __ldcg(a.xc + __ldg(a.aggp + i));  // prolongation (k_prolong)
-  __syncthreads();
-  lv_pass<0>(a, a.nc - 1, -1, a.nc, sx);
-  for (int i = threadIdx.x; i < a.n; i += LV_THREADS) a.x[i] = sx[i];
-  mk.end();
-}
-
-static LvArgs lv_args(const cprb_amg_level& L) {
-  LvArgs a = {};
-  a.S = L.smoother;
-  a.R = L.restrict_op;
-  a.diag = L.diag;
-  a.aggp = L.aggp;
-  a.b = L.b;
-  a.x = L.x;
-  a.n = L.n;
-  a.nc = L.ncolors;
-  for (int k = 0; k <= L.ncolors && k <= LV_MAXC; ++k) {
-    a.cs[k] = L.color_slices[k];
-    a.cr[k] = L.color_rows[k];
-  }
-  return a;
-}
-
-static bool lv_ok(const cprb_amg_level& L) {
-  if (!L.one_cta || L.ncolors < 2 || L.ncolors > LV_MAXC) return false;
-  if ((size_t)L.n * sizeof(double) > 200 * 1024) return false;
-  if (L.color_snapshot)
-    for (int k = 0; k < L.ncolors; ++k)
-      if (L.color_snapshot[k]) return false;
-  return true;
-}
-
-static void lv_attr() {
-  static bool done = false;
-  if (!done) {
-    cudaFuncSetAttribute(k_lv_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_lv_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    done = true;
-  }
-}
-
 int amg_vcycle(const cprb_amg& h, const double* r, double* z, cudaStream_t st) {
+  NvtxRange nv("amg_vcycle");
   const int nl = h.nlevels;
   if (nl <= 1) {
     k_gather<<<nblk(h.n_coarse, 256), 256, 0, st>>>(h.n_coarse, nullptr, r, h.in_stride, h.coarse_b);
@@ -898,26 +455,13 @@ int amg_vcycle(const cprb_amg& h, const double* r, double* z, cudaStream_t st) {
                                                                      h.coarse_b, z, nullptr);
     return check_launch("coarse-only cycle");
   }
-  const bool tail = h.tail_mode == 3 && h.tail3_buf && h.tail_levels && h.tail_phases &&
-                    h.tail_nphases > 0 && h.tail_start >= 1 && h.tail_start < nl - 1;
+  // levels >= ts (and the coarse solve) run in the persistent tail
+  const bool tail = h.tail_start >= 1 && h.tail_start < nl - 1 && h.tail_nphases > 0 &&
+                    h.tail_stream && h.tail_phases && h.tail_chunks && h.tail_vec;
   const int ts = tail ? h.tail_start : nl - 1;
   int fused = 0;  // colour 0 of this level was computed by the previous restriction
   for (int l = 0; l < ts; ++l) {
     const cprb_amg_level& L = h.levels[l];
-    if (l >= 1 && lv_ok(L)) {
-      lv_attr();
-      LvArgs a = lv_args(L);
-      a.fused = fused;
-      a.bc = (l + 1 < nl - 1) ? h.levels[l + 1].b : h.coarse_b;
-      const cprb_amg_level* next =
-          (l + 1 < ts && h.levels[l + 1].ncolors > 1) ? &h.levels[l + 1] : nullptr;
-      a.xn = next ? next->x : nullptr;
-      a.dn = next ? next->diag : nullptr;
-      a.c0n = next ? next->color_rows[1] : 0;
-      launch_pdl(k_lv_fwd, 1, LV_THREADS, (size_t)L.n * sizeof(double), st, a);
-      fused = next ? 1 : 0;
-      continue;
-    }
     int rc = pgs_pass(L, L.b, L.x, 0, 1, l == 0 ? r : nullptr, h.in_stride, h.perm0, nullptr, st,
                       fused);
     if (rc) return rc;
@@ -927,7 +471,7 @@ int amg_vcycle(const cprb_amg& h, const double* r, double* z, cudaStream_t st) {
     fused = next ? 1 : 0;
   }
   if (tail) {
-    int rc = launch_vtail3(h, st);
+    int rc = launch_vtail(h, st);
     if (rc) return rc;
   } else {
     launch_pdl(k_dense_mv, nblk((int64_t)h.n_coarse * 32, 256), 256, 0, st, h.n_coarse,
@@ -936,12 +480,6 @@ int amg_vcycle(const cprb_amg& h, const double* r, double* z, cudaStream_t st) {
   for (int l = ts - 1; l >= 0; --l) {
     const cprb_amg_level& L = h.levels[l];
     const double* xc = (l + 1 < nl - 1) ? h.levels[l + 1].x : h.coarse_x;
-    if (l >= 1 && lv_ok(L)) {
-      LvArgs a = lv_args(L);
-      a.xc = xc;
-      launch_pdl(k_lv_bwd, 1, LV_THREADS, (size_t)L.n * sizeof(double), st, a);
-      continue;
-    }
     launch_pdl(k_prolong, nblk(L.n, 256), 256, 0, st, L.n, L.aggp, xc, L.x);
     int rc = pgs_pass(L, L.b, L.x, 1, 0, nullptr, 0, h.perm0, l == 0 ? z : nullptr, st);
     if (rc) return rc;
@@ -952,12 +490,6 @@ int amg_vcycle(const cprb_amg& h, const double* r, double* z, cudaStream_t st) {
 }  // namespace cprb
 
 using namespace cprb;
-
-extern "C" int cprb_tail3_set_log(uint64_t* dev_log) {
-  unsigned long long* p = (unsigned long long*)dev_log;
-  cudaMemcpyToSymbol(cprb::g_tail3_log, &p, sizeof(p));
-  return check_launch("tail3 log");
-}
 
 extern "C" int cprb_amg_set_log(uint64_t* dev_log) {
   unsigned long long* p = (unsigned long long*)dev_log;

@@ -40,6 +40,7 @@ int stencil_solve(const cprb_bilu& F, const double* rhsL, cudaStream_t st);
 int wave_combine(const cprb_bilu& F, const double* zp, double* z, cudaStream_t st);
 int wave_scatter_rhs(const cprb_bilu& F, const double* r, double* rhsL, cudaStream_t st);
 int amg_vcycle(const cprb_amg& h, const double* r, double* z, cudaStream_t st);
+int launch_vtail(const cprb_amg& h, cudaStream_t st);
 int kcycle_apply(const cprb_amg& h, const double* r, double* z, cudaStream_t st);
 int bilu_solve(const cprb_bilu& F, const double* r, double* zl, double* y, const double* zp,
                double* zout, cudaStream_t st);

@@ -8,11 +8,15 @@
 // (cprb_dot), IEEE scalar divisions and separately rounded axpys, so the
 // device and host K-cycles agree bitwise.
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 #include <string>
 #include <vector>
 
 #include "device.cuh"
 #include "engine.h"
+#include "ktail.h"
+#include "nvtx.h"
 
 namespace cprb {
 
@@ -190,6 +194,11 @@ struct KPlan {
   int32_t* ticket = nullptr;
   std::vector<void*> allocs;
   int pre = 1, post = 1;
+  // persistent tail (csrc/ktail.cu): Krylov frames at levels >= kt_start run
+  // in one CTA; kt_start >= nl - 1 disables it
+  KTDesc* kt_dev = nullptr;
+  int kt_start = 1 << 30;
+  int kt_threads = 1024;
 
   double* alloc(size_t n_) {
     void* p = nullptr;
@@ -310,8 +319,9 @@ static int kcycle_at(const KPlan& P, const cprb_amg& h, int l, const double* b, 
                                                            P.coarse_x);
     ec = P.coarse_x;
   } else {
-    if ((rc = (h.use_fcg ? fcg_at(P, h, l + 1, bc, st) : fgmres_at(P, h, l + 1, bc, st))))
-      return rc;
+    if (l + 1 >= P.kt_start) rc = ktail_launch(P.kt_dev, P.kt_threads, l + 1, bc, st);
+    else rc = h.use_fcg ? fcg_at(P, h, l + 1, bc, st) : fgmres_at(P, h, l + 1, bc, st);
+    if (rc) return rc;
     ec = P.x[l + 1];
   }
   k_kprolong<<<kfull(Lv.n), 256, 0, st>>>(Lv.n, Lv.aggp, ec, x);
@@ -321,6 +331,7 @@ static int kcycle_at(const KPlan& P, const cprb_amg& h, int l, const double* b, 
 }
 
 int kcycle_apply(const cprb_amg& h, const double* r, double* z, cudaStream_t st) {
+  NvtxRange nv("amg_kcycle");
   const KPlan* P = static_cast<const KPlan*>((void*)h.kwork);
   if (!P) return set_error(CPRB_EINVAL, "K-cycle plan missing (cprb_kcycle_create)");
   if (h.nlevels <= 1) {
@@ -334,6 +345,67 @@ int kcycle_apply(const cprb_amg& h, const double* r, double* z, cudaStream_t st)
   if (rc) return rc;
   k_kscatter<<<kfull(n0), 256, 0, st>>>(n0, h.perm0, P->x0[0], z);
   return check_launch("k cycle apply");
+}
+
+// Persistent tail plan: the first level l >= 1 with at most CPRB_KTAIL_ROWS
+// rows (default 0 = off) such that every level from l on fits the
+// tail's limits.  CPRB_KTAIL_THREADS = 512 | 1024 (default) sizes the CTA.
+static int ktail_plan(KPlan& P, const cprb_amg& h) {
+  const int L = h.nlevels;
+  long thr = 0;
+  if (const char* e = getenv("CPRB_KTAIL_ROWS")) thr = atol(e);
+  if (const char* e = getenv("CPRB_KTAIL_THREADS")) P.kt_threads = atoi(e) == 512 ? 512 : 1024;
+  if (thr <= 0 || L < 3 || L - 1 > KT_MAXL) return CPRB_OK;
+  int start = -1;
+  for (int l = L - 2; l >= 1; --l) {
+    const cprb_amg_level& Lv = h.levels[l];
+    if (Lv.n > thr || Lv.n > KT_MAXVB * 1024 || Lv.ncolors > KT_MAXC || Lv.ncolors < 1) break;
+    start = l;
+  }
+  if (start < 1 || L - 1 - start > KT_MAXD) return CPRB_OK;
+  KTDesc d;
+  memset(&d, 0, sizeof(d));
+  d.L = L;
+  d.start = start;
+  d.pre = P.pre;
+  d.post = P.post;
+  d.use_fcg = h.use_fcg;
+  d.n_coarse = h.n_coarse;
+  d.coarse_inv = h.coarse_inv;
+  d.coarse_x = P.coarse_x;
+  for (int l = start - 1; l < L - 1; ++l) {
+    const cprb_amg_level& Lv = h.levels[l];
+    KTLevel& t = d.lv[l];
+    t.sm = Lv.smoother;
+    t.rop = Lv.restrict_op;
+    if (l >= 1) t.A = P.spmv[l];
+    t.diag = Lv.diag;
+    t.aggp = Lv.aggp;
+    t.x = P.x[l]; t.r = P.r[l]; t.z1 = P.z1[l]; t.ap1 = P.ap1[l];
+    t.z2 = P.z2[l]; t.p2 = P.p2[l]; t.ap2 = P.ap2[l];
+    t.tmp = Lv.tmp;
+    t.rc = P.rc[l];
+    t.n = Lv.n;
+    t.nc = Lv.ncolors;
+    t.snap = 0;
+    if (l >= start) {
+      for (int k = 0; k <= Lv.ncolors; ++k) {
+        t.cr[k] = Lv.color_rows[k];
+        t.cs[k] = Lv.color_slices[k];
+      }
+      for (int k = 0; k < Lv.ncolors; ++k)
+        if (Lv.color_snapshot && Lv.color_snapshot[k]) t.snap |= 1u << k;
+    }
+  }
+  void* dd = nullptr;
+  if (cudaMalloc(&dd, sizeof(KTDesc)) != cudaSuccess)
+    return set_error(CPRB_EDEVICE, "K-cycle tail plan allocation");
+  P.allocs.push_back(dd);
+  if (cudaMemcpy(dd, &d, sizeof(KTDesc), cudaMemcpyHostToDevice) != cudaSuccess)
+    return set_error(CPRB_EDEVICE, "K-cycle tail plan upload");
+  P.kt_dev = (KTDesc*)dd;
+  P.kt_start = start;
+  return CPRB_OK;
 }
 
 }  // namespace cprb
@@ -385,6 +457,10 @@ int cprb_kcycle_create(const cprb_amg* h, const cprb_sell* level_spmv, int32_t p
       delete P;
       return set_error(CPRB_EDEVICE, "K-cycle workspace allocation");
     }
+  if (int rc = ktail_plan(*P, *h)) {
+    delete P;
+    return rc;
+  }
   cudaDeviceSynchronize();
   *out = P;
   return check_launch("kcycle create");
@@ -410,7 +486,9 @@ int cprb_kcycle_correction(const cprb_amg* h, int32_t l, const int32_t* perm, co
                                                               P->coarse_x);
     xl = P->coarse_x;
   } else {
-    const int rc = h->use_fcg ? fcg_at(*P, *h, l, bl, st) : fgmres_at(*P, *h, l, bl, st);
+    const int rc = l >= P->kt_start ? ktail_launch(P->kt_dev, P->kt_threads, l, bl, st)
+                   : h->use_fcg     ? fcg_at(*P, *h, l, bl, st)
+                                    : fgmres_at(*P, *h, l, bl, st);
     if (rc) return rc;
     xl = P->x[l];
   }

@@ -7,6 +7,7 @@
 
 #include "device.cuh"
 #include "engine.h"
+#include "nvtx.h"
 
 namespace cprb {
 
@@ -183,6 +184,7 @@ int cprb_dot(int64_t n, const double* x, const double* y, double* out, double* p
 
 int cprb_arnoldi_mgs(int64_t n, int32_t j, double* V, int64_t ldv, double* Hcol,
                      double* partials, int32_t* ticket, void* stream) {
+  NvtxRange nv("arnoldi_mgs");
   cudaStream_t st = (cudaStream_t)stream;
   double* w = V + (int64_t)(j + 1) * ldv;
   const int g = red_blocks(n);
@@ -224,6 +226,7 @@ int cprb_div_scalar(int64_t n, const double* x, const double* h_dev, double* out
 
 // src/cpr.py:184-186 given zp in P->zp:  r2 = r - A Pi zp;  z = Pi zp + BILU(r2)
 int cprb_cpr_finish(const cprb_cpr* P, const double* r, double* z, void* stream) {
+  NvtxRange nv("cpr_stage2_bilu");
   cudaStream_t st = (cudaStream_t)stream;
   const cprb_bilu& F = P->bilu;
   if (F.use_wave) {
@@ -245,6 +248,7 @@ int cprb_cpr_finish(const cprb_cpr* P, const double* r, double* z, void* stream)
 
 // src/cpr.py:178-186:  zp = AMG(Pi^T r);  r2 = r - A Pi zp;  z = Pi zp + BILU(r2)
 int cprb_cpr_apply(const cprb_cpr* P, const double* r, double* z, void* stream) {
+  NvtxRange nv("cpr_apply");
   int rc = P->amg.cycle != 0 ? kcycle_apply(P->amg, r, P->zp, (cudaStream_t)stream)
                              : amg_vcycle(P->amg, r, P->zp, (cudaStream_t)stream);
   if (rc) return rc;

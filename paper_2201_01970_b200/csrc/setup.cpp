@@ -353,6 +353,66 @@ inline void matmul(int b, const double* x, const double* y, double* out) {
     }
 }
 
+// BILU(0) rows with a compile-time block size: the generic loop below with
+// matmul/gj_invert unrolled -- the same operations in the same order, so the
+// factors are bitwise those of the runtime-b path
+template <int B>
+inline void matmul_t(const double* x, const double* y, double* out) {
+  for (int i = 0; i < B; ++i)
+    for (int l = 0; l < B; ++l) {
+      double s = 0.0;
+      for (int j = 0; j < B; ++j) s = s + x[i * B + j] * y[j * B + l];
+      out[i * B + l] = s;
+    }
+}
+
+template <int B>
+int bilu0_rows(int64_t n, const int64_t* ptr, const int64_t* cols, double* vals, double* uinv,
+               int64_t* perturbed, int64_t* n_perturbed) {
+  constexpr int BB = B * B;
+  int64_t npert = 0;
+  double tmp[BB];
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t lo = ptr[i], hi = ptr[i + 1];
+    const int64_t* rb = cols + lo;
+    const int64_t dk = std::lower_bound(rb, cols + hi, i) - rb;
+    if (lo + dk >= hi || cols[lo + dk] != i)
+      return set_error(CPRB_EINVAL, "diagonal block missing in row " + std::to_string(i));
+    for (int64_t p = lo; p < lo + dk; ++p) {
+      const int64_t k = cols[p];
+      matmul_t<B>(vals + p * BB, uinv + k * BB, tmp);
+      std::memcpy(vals + p * BB, tmp, sizeof(double) * BB);
+      const int64_t klo = ptr[k], khi = ptr[k + 1];
+      int64_t pos = klo;
+      for (int64_t q = p + 1; q < hi; ++q) {
+        const int64_t j = cols[q];
+        while (pos < khi && cols[pos] < j) ++pos;
+        if (pos < khi && cols[pos] == j) {
+          matmul_t<B>(vals + p * BB, vals + pos * BB, tmp);
+          for (int e = 0; e < BB; ++e) vals[q * BB + e] = vals[q * BB + e] - tmp[e];
+        }
+      }
+    }
+    const double* piv = vals + (lo + dk) * BB;
+    if (!gj_invert(B, piv, uinv + i * BB)) {
+      double sq[BB];
+      for (int e = 0; e < BB; ++e) sq[e] = piv[e] * piv[e];
+      const double fro = std::sqrt(pairwise_sum(sq, BB));
+      if (fro == 0.0)
+        return set_error(CPRB_ESINGULAR, "singular pivot block at row " + std::to_string(i));
+      const double t = 1e-8 * fro;
+      double bumped[BB];
+      for (int r = 0; r < B; ++r)
+        for (int c = 0; c < B; ++c) bumped[r * B + c] = piv[r * B + c] + (r == c ? t * 1.0 : t * 0.0);
+      if (!gj_invert(B, bumped, uinv + i * BB))
+        return set_error(CPRB_ESINGULAR, "singular pivot block at row " + std::to_string(i));
+      perturbed[npert++] = i;
+    }
+  }
+  *n_perturbed = npert;
+  return CPRB_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -370,6 +430,7 @@ int cprb_bilu0_factorize(int64_t n, int32_t b, const int64_t* ptr, const int64_t
                          double* vals, double* uinv, int64_t* perturbed,
                          int64_t* n_perturbed) {
   if (b < 1 || b > 8) return set_error(CPRB_EINVAL, "block size must be 1..8");
+  if (b == 3) return bilu0_rows<3>(n, ptr, cols, vals, uinv, perturbed, n_perturbed);
   const int bb = b * b;
   int64_t npert = 0;
   double tmp[64];
@@ -438,6 +499,61 @@ int cprb_level_schedule(int64_t n, const int64_t* ptr, const int64_t* cols, int6
   }
   *nlevels = n > 0 ? maxl : 1;
   return CPRB_OK;
+}
+
+// Level schedule of the STRICT LOWER part of a pattern that may hold both
+// triangles (A's own pattern): level(i) = 1 + max level(j), j < i in row i.
+// The BILU(0) factorization's row dependencies (src/ilu.py:150-193); equal
+// to cprb_level_schedule on the factor L's pattern.
+int cprb_lower_level_schedule(int64_t n, const int64_t* ptr, const int64_t* cols, int64_t* level,
+                              int64_t* nlevels) {
+  int64_t maxl = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t m = 0;
+    for (int64_t p = ptr[i]; p < ptr[i + 1]; ++p)
+      if (cols[p] < i) m = std::max(m, level[cols[p]]);
+    level[i] = 1 + m;
+    maxl = std::max(maxl, level[i]);
+  }
+  *nlevels = n > 0 ? maxl : 1;
+  return CPRB_OK;
+}
+
+// Structured-grid detection for the stencil BILU plan (ilu.py stencil_plan):
+// n = nx*ny*nz with x fastest and every row's block columns exactly the
+// in-range 7-point neighbours, ascending (-z, -y, -x, i, +x, +y, +z).
+// dims[0..2] = nx, ny, nz on success; returns 0 when the pattern is not such
+// a grid (dims untouched), 1 when it is.
+int cprb_detect_stencil(int64_t n, const int64_t* ptr, const int64_t* cols, int64_t* dims) {
+  if (n < 8) return 0;
+  // nx = distance to the first +y neighbour of row 0 = (col of the third
+  // upper entry of row 0 when all three exist) -- derive from row 0: cols
+  // 0, 1, nx, nxy
+  if (ptr[1] - ptr[0] != 4) return 0;
+  const int64_t nx = cols[ptr[0] + 2], nxy = cols[ptr[0] + 3];
+  if (cols[ptr[0]] != 0 || cols[ptr[0] + 1] != 1 || nx < 2 || nxy <= nx || nxy % nx || n % nxy)
+    return 0;
+  const int64_t ny = nxy / nx, nz = n / nxy;
+  if (ny < 2 || nz < 2) return 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t ix = i % nx, iy = (i / nx) % ny, iz = i / nxy;
+    int64_t want[7];
+    int k = 0;
+    if (iz > 0) want[k++] = i - nxy;
+    if (iy > 0) want[k++] = i - nx;
+    if (ix > 0) want[k++] = i - 1;
+    want[k++] = i;
+    if (ix + 1 < nx) want[k++] = i + 1;
+    if (iy + 1 < ny) want[k++] = i + nx;
+    if (iz + 1 < nz) want[k++] = i + nxy;
+    if (ptr[i + 1] - ptr[i] != k) return 0;
+    for (int t = 0; t < k; ++t)
+      if (cols[ptr[i] + t] != want[t]) return 0;
+  }
+  dims[0] = nx;
+  dims[1] = ny;
+  dims[2] = nz;
+  return 1;
 }
 
 // Coarsest solve operator: inverse of a dense n x n matrix via LU with

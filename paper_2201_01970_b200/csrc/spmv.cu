@@ -5,6 +5,7 @@
 // (src/sparse.py:322-351 via src/_kernels.py:17-45).
 #include "device.cuh"
 #include "engine.h"
+#include "nvtx.h"
 
 namespace cprb {
 
@@ -118,6 +119,7 @@ static void launch_bsr(const cprb_sell& A, const double* x, const double* rhs, d
 int bsr_op(int mode, const cprb_sell& A, int b, const double* x, const double* rhs, double* out,
            int32_t* flag, double* sent, cudaStream_t st, const int32_t* oi, double* sent2,
            const int32_t* si, const int32_t* si2) {
+  NvtxRange nv(mode == 0 ? "bsr_spmv" : (mode == 1 ? "bsr_residual" : "bsr_stage2_residual"));
   if (b == 3) {
     if (mode == 0) launch_bsr<3, 0>(A, x, rhs, out, flag, sent, sent2, st, oi, si, si2);
     else if (mode == 1) launch_bsr<3, 1>(A, x, rhs, out, flag, sent, sent2, st, oi, si, si2);

@@ -36,6 +36,7 @@
 
 #include "device.cuh"
 #include "engine.h"
+#include "nvtx.h"
 #include "tma.cuh"
 
 namespace cg = cooperative_groups;
@@ -481,6 +482,7 @@ static int launch_stencil(const cprb_stencil& T, const double* rhs, double* out,
 // F.zl_step and F.y_step must be sentinel-armed; y is left in stencil
 // order in F.y_step (z = Pi zp + y gathers it through F.u_slot).
 int stencil_solve(const cprb_bilu& F, const double* rhsL, cudaStream_t st) {
+  NvtxRange nv("bilu_stencil_solve");
   if (F.b != 3) return set_error(CPRB_EUNSUPPORTED, "stencil BILU needs 3x3 blocks");
   if (cudaMemsetAsync(F.tickets + 4, 0, 2 * sizeof(int32_t), st) != cudaSuccess)
     return check_launch("stencil tickets");

@@ -25,6 +25,7 @@
 #include "device.cuh"
 #include "tma.cuh"
 #include "engine.h"
+#include "nvtx.h"
 
 namespace cprb {
 
@@ -511,6 +512,7 @@ __global__ void k_l_to_u(int n, int b, const int32_t* __restrict__ ls, const int
 // L solve -> permute -> U solve.  rhsL: r in L-step order; F.zl_step and
 // F.y_step must be sentinel-armed; y is left in U-step order in F.y_step.
 int wave_solve(const cprb_bilu& F, const double* rhsL, cudaStream_t st) {
+  NvtxRange nv("bilu_wave_solve");
   int rc;
   const int blocks = (F.n + 255) / 256 < 4 * 148 ? (F.n + 255) / 256 : 4 * 148;
   if (F.b == 3) {

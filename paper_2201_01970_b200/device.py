@@ -39,6 +39,23 @@ def stream() -> int:
     return torch().cuda.current_stream().cuda_stream
 
 
+def bind_current(fn):
+    """Wrap fn so that, run on a setup-pool thread, it uses the caller's CUDA
+    device and stream (torch keeps both per thread)."""
+    t = torch()
+    dev = t.cuda.current_device()
+    st = t.cuda.current_stream()
+
+    def run(*args, **kw):
+        with t.cuda.device(dev), t.cuda.stream(st):
+            return fn(*args, **kw)
+    return run
+
+
+def is_tensor(a) -> bool:
+    return type(a).__module__.startswith("torch")
+
+
 def ptr(t) -> int:
     return 0 if t is None else int(t.data_ptr())
 
@@ -222,7 +239,7 @@ class _PackedSell:
     new Jacobian is one H2D copy of the CSR plus one kernel, not a host
     repack.  Same layout and values as sell_rows()."""
 
-    def __init__(self, A, bs: int):
+    def __init__(self, A, bs: int, dev_csr=None):
         t = torch()
         n = int(A.nrows)
         rp = np.ascontiguousarray(A.row_ptr, dtype=np.int64)
@@ -244,9 +261,12 @@ class _PackedSell:
                   "vals": t.zeros(max(total * bb, 1), dtype=t.float64, device="cuda")}
         nnz = int(rp[-1])
         if n and nnz:
-            rp_d = upload(rp)
-            ci_d = upload(np.ascontiguousarray(A.col_idx, dtype=np.int64))
-            v_d = upload(np.ascontiguousarray(A.values, dtype=np.float64).reshape(-1))
+            if dev_csr is not None:        # CSR already in HBM (device generator)
+                rp_d, ci_d, v_d = dev_csr
+            else:
+                rp_d = upload(rp)
+                ci_d = upload(np.ascontiguousarray(A.col_idx, dtype=np.int64))
+                v_d = upload(np.ascontiguousarray(A.values, dtype=np.float64).reshape(-1))
             N.check(N.lib().cprb_pack_bsr_sell(n, bs, ptr(rp_d), ptr(ci_d), ptr(v_d),
                                                ptr(self.t["slice_ptr"]), ptr(self.t["cols"]),
                                                ptr(self.t["vals"]), stream()))
@@ -262,25 +282,53 @@ class _PackedSell:
 class DeviceMatrix:
     """A CsrMatrix / BlockCsrMatrix resident on the device (SELL-32)."""
 
-    def __init__(self, A):
+    def __init__(self, A, dev_csr=None):
         require_cuda()
         bs = int(getattr(A, "block_size", 1))
         self.b = bs
         self.nrows = int(A.nrows)
-        self.sell = _PackedSell(A, bs)
+        self.sell = _PackedSell(A, bs, dev_csr)
+        # the CSR itself when it was born on the device (device generator):
+        # the device BILU(0) factorization starts from it without an upload
+        self.csr = dev_csr
 
     def desc_ref(self):
         return C.byref(self.sell.desc)
 
 
-def device_matrix(A) -> DeviceMatrix:
+def device_matrix(A, dev_csr=None) -> DeviceMatrix:
     """Device copy cached on the matrix object (matrices are immutable after
-    construction in the reference's contract, src/sparse.py:217-218)."""
+    construction in the reference's contract, src/sparse.py:217-218).
+    dev_csr = (row_ptr, col_idx, values) already on the device: packed
+    without an upload.  release_device(A) drops the cached copy."""
     M = getattr(A, "_cprb_dev", None)
     if M is None:
-        M = DeviceMatrix(A)
+        M = DeviceMatrix(A, dev_csr)
         try:
             object.__setattr__(A, "_cprb_dev", M)
         except (AttributeError, TypeError):
             pass
     return M
+
+
+def cuda_ok() -> bool:
+    """A CUDA device and the native library are both available."""
+    try:
+        if not torch().cuda.is_available():
+            return False
+        N.lib()
+        return True
+    except (ImportError, OSError, RuntimeError):
+        return False
+
+
+def cached_device_matrix(A):
+    return getattr(A, "_cprb_dev", None)
+
+
+def release_device(A) -> None:
+    """Free the device copy cached on A (it is rebuilt on the next use)."""
+    try:
+        object.__setattr__(A, "_cprb_dev", None)
+    except (AttributeError, TypeError):
+        pass

@@ -20,7 +20,8 @@ from . import _native as N
 from . import device as D
 from .sparse import BlockCsrMatrix, CsrMatrix, to_block
 
-__all__ = ["BiluFactors", "LevelSchedule", "bilu0_factorize", "level_schedule", "bilu_apply"]
+__all__ = ["BiluFactors", "DeviceBiluFactors", "LevelSchedule", "bilu0_factorize",
+           "bilu0_factorize_device", "level_schedule", "bilu_apply"]
 
 
 @dataclass
@@ -95,6 +96,12 @@ def bilu0_factorize(A) -> BiluFactors:
                                          N.p64(pert), N.p64(npert)))
     for row in pert[:int(npert[0])]:
         N.warn(f"bilu0: perturbing singular pivot block at row {int(row)}", RuntimeWarning, 2)
+    return _factors_from(n, b, ptr, cols, vals, uinv)
+
+
+def _factors_from(n, b, ptr, cols, vals, uinv) -> BiluFactors:
+    """Split the in-place factored values on A's pattern into L (strict
+    lower + identity diagonal) and U (diagonal + strict upper)."""
     rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(ptr))
     lower = cols < rows
     # L: strict lower then the identity diagonal (already column-sorted per row)
@@ -115,6 +122,110 @@ def bilu0_factorize(A) -> BiluFactors:
     np.cumsum(np.bincount(rows[~lower], minlength=n), out=uptr[1:])
     U = BlockCsrMatrix(b, n, n, uptr, cols[~lower].copy(), vals[~lower].copy())
     return BiluFactors(L, U, b, uinv, level_schedule(L), level_schedule(U))
+
+
+class DeviceBiluFactors(BiluFactors):
+    """BILU(0) factored ON THE DEVICE (csrc/factor.cu): the factors stay in
+    HBM on A's pattern; the stencil plan of the solves is packed from them
+    on the device.  The host view (L, U, u_diag_inv, schedules -- the
+    reference's BiluFactors fields) is downloaded on first access and is
+    bitwise the host factorization's."""
+
+    def __init__(self, n, b, ptr, cols, csr_d, vals_d, uinv_d):
+        self._n, self._b = int(n), int(b)
+        self.ptr, self.cols = ptr, cols
+        self.csr_d = csr_d            # (row_ptr, col_idx) on the device
+        self.vals_d, self.uinv_d = vals_d, uinv_d
+        self._host = None
+        self._dev = None
+
+    def _h(self) -> BiluFactors:
+        if self._host is None:
+            vals = self.vals_d.cpu().numpy().reshape(-1, self._b, self._b)
+            uinv = self.uinv_d.cpu().numpy().reshape(-1, self._b, self._b)
+            self._host = _factors_from(self._n, self._b, self.ptr, self.cols, vals, uinv)
+        return self._host
+
+    L = property(lambda self: self._h().L)
+    U = property(lambda self: self._h().U)
+    u_diag_inv = property(lambda self: self._h().u_diag_inv)
+    l_schedule = property(lambda self: self._h().l_schedule)
+    u_schedule = property(lambda self: self._h().u_schedule)
+    block_size = property(lambda self: self._b)
+
+    @property
+    def n(self) -> int:
+        return self._n
+
+    def __repr__(self):
+        return f"DeviceBiluFactors(n={self._n}, block_size={self._b})"
+
+    def stencil_device(self):
+        """Stencil plan (as stencil_plan) packed on the device, or None."""
+        if self._b != 3:
+            return None
+        dims = np.zeros(3, dtype=np.int64)
+        if not N.lib().cprb_detect_stencil(self._n, N.p64(self.ptr), N.p64(self.cols), N.p64(dims)):
+            return None
+        nx, ny, nz = (int(v) for v in dims)
+        if nx > 32 * STENCIL_SMAX:
+            return None
+        doff, P = _stencil_offsets(nx, ny)
+        t = D.torch()
+        lrec = t.zeros(nz * P * 27, dtype=t.float64, device="cuda")
+        urec = t.zeros(nz * P * 37, dtype=t.float64, device="cuda")
+        slot = t.empty(self._n, dtype=t.int32, device="cuda")
+        doff_d = D.upload(doff.astype(np.int32))
+        N.check(N.lib().cprb_stencil_pack(self._n, nx, ny, P, D.ptr(doff_d), D.ptr(self.csr_d[0]),
+                                          D.ptr(self.csr_d[1]), D.ptr(self.vals_d),
+                                          D.ptr(self.uinv_d), D.ptr(lrec), D.ptr(urec),
+                                          D.ptr(slot), D.stream()))
+        return {"nx": nx, "ny": ny, "nz": nz, "S": (nx + 31) // 32, "D": nx + ny - 1, "P": P,
+                "doff": doff_d, "lrec": lrec, "urec": urec, "slot": slot, "len": 3 * nz * P}
+
+
+def bilu0_factorize_device(A, dev_csr=None) -> DeviceBiluFactors:
+    """src/ilu.py:150-193 on the device (3x3 blocks): the factorization runs
+    level by level over the strict-lower dependency schedule
+    (csrc/factor.cu), bitwise the host C++ factorization; errors and the
+    perturbation warnings are the host path's.  dev_csr = (row_ptr,
+    col_idx, values) already in HBM (e.g. from the device generator)."""
+    b = int(getattr(A, "block_size", 1))
+    n = A.nrows
+    if A.nrows != A.ncols:
+        raise ValueError("factorization needs a square matrix")
+    ptr = np.ascontiguousarray(A.row_ptr, dtype=np.int64)
+    cols = np.ascontiguousarray(A.col_idx, dtype=np.int64)
+    level = np.zeros(max(n, 1), dtype=np.int64)
+    nl = np.zeros(1, dtype=np.int64)
+    N.check(N.lib().cprb_lower_level_schedule(n, N.p64(ptr), N.p64(cols if cols.size else level),
+                                              N.p64(level), N.p64(nl)))
+    nlev = int(nl[0])
+    order = np.argsort(level[:n], kind="stable").astype(np.int32)
+    lptr = np.zeros(nlev + 1, dtype=np.int64)
+    np.cumsum(np.bincount(level[:n], minlength=nlev + 1)[1:], out=lptr[1:])
+    t = D.torch()
+    if dev_csr is None:
+        dev_csr = (D.upload(ptr), D.upload(cols),
+                   D.upload(np.ascontiguousarray(A.values, dtype=np.float64).reshape(-1)))
+    vals_d = dev_csr[2].clone()
+    uinv_d = t.zeros(n * b * b, dtype=t.float64, device="cuda")
+    err = t.zeros(4, dtype=t.int32, device="cuda")
+    pert = t.zeros(max(n, 1), dtype=t.int64, device="cuda")
+    rows_d = D.upload(order)
+    N.check(N.lib().cprb_bilu0_factorize_device(n, b, D.ptr(dev_csr[0]), D.ptr(dev_csr[1]),
+                                                D.ptr(vals_d), D.ptr(uinv_d), D.ptr(rows_d),
+                                                N.p64(lptr), nlev, D.ptr(err), D.ptr(pert),
+                                                D.stream()))
+    e = err.cpu().numpy()
+    bad_diag, bad_piv = int(e[1]), int(e[0])
+    if min(bad_diag, bad_piv) < 2**31 - 1:
+        if bad_diag < bad_piv:
+            raise ValueError(f"diagonal block missing in row {bad_diag}")
+        raise np.linalg.LinAlgError(f"singular pivot block at row {bad_piv}")
+    for row in np.sort(pert[:int(e[2])].cpu().numpy()):
+        N.warn(f"bilu0: perturbing singular pivot block at row {int(row)}", RuntimeWarning, 2)
+    return DeviceBiluFactors(n, b, ptr, cols, dev_csr[:2], vals_d, uinv_d)
 
 
 def _strict(T: BlockCsrMatrix):
@@ -316,6 +427,20 @@ def wave_plan(T: BlockCsrMatrix, sched: LevelSchedule, b: int, upper: bool, uinv
 STENCIL_SMAX = 4   # x-segments of 32 lanes per warp (csrc/stencil.cu): nx <= 128
 
 
+def _stencil_offsets(nx, ny):
+    """Padded offsets of the anti-diagonals d = ix + iy of one xy-plane
+    (widths rounded up to even: 16-byte TMA granules) and the plane size."""
+    Dn = nx + ny - 1
+    d = np.arange(Dn, dtype=np.int64)
+    lo = np.maximum(0, d - (ny - 1))
+    hi = np.minimum(nx - 1, d)
+    w = hi - lo + 1
+    wp = w + (w & 1)
+    doff = np.zeros(Dn + 1, dtype=np.int64)
+    np.cumsum(wp, out=doff[1:])
+    return doff, int(doff[-1])
+
+
 def stencil_plan(F: BiluFactors):
     """Structured-grid plan of the BILU(0) solves (csrc/stencil.cu), or None.
 
@@ -356,15 +481,9 @@ def stencil_plan(F: BiluFactors):
     exp_u = (i[:, None] + ou[None, :])[hu]
     if not (np.array_equal(exp_l, lc) and np.array_equal(exp_u, uc)):
         return None
+    doff, P = _stencil_offsets(nx, ny)
     Dn = nx + ny - 1
-    d = np.arange(Dn, dtype=np.int64)
-    lo = np.maximum(0, d - (ny - 1))
-    hi = np.minimum(nx - 1, d)
-    w = hi - lo + 1
-    wp = w + (w & 1)
-    doff = np.zeros(Dn + 1, dtype=np.int64)
-    np.cumsum(wp, out=doff[1:])
-    P = int(doff[-1])
+    lo = np.maximum(0, np.arange(Dn, dtype=np.int64) - (ny - 1))
     dc = ix + iy
     j = ix - lo[dc]
     pos = iz * P + doff[dc] + j                       # stencil position of every row
@@ -410,7 +529,7 @@ class DeviceBilu:
         self.use_wave = bool(F.n > 0 and use_wave)
         st = None
         if self.use_wave and os.environ.get("CPRB_STENCIL", "1") != "0":
-            st = stencil_plan(F)
+            st = F.stencil_device() if isinstance(F, DeviceBiluFactors) else stencil_plan(F)
         self.stencil = st is not None
         if self.use_wave:
             # the wave plans carry their own copies of the factors; the
@@ -434,10 +553,11 @@ class DeviceBilu:
             # structured grid: one warp per xy-plane sweeping anti-diagonals
             # (csrc/stencil.cu); rhs, L output and U output share the layout
             self.Lw = self.Uw = None
-            self.st_doff = D.upload(st["doff"])
-            self.st_lrec = D.upload(st["lrec"])
-            self.st_urec = D.upload(st["urec"])
-            self.l_slot = self.u_slot = D.upload(st["slot"])
+            up = lambda a: a if D.is_tensor(a) else D.upload(a)   # noqa: E731
+            self.st_doff = up(st["doff"])
+            self.st_lrec = up(st["lrec"])
+            self.st_urec = up(st["urec"])
+            self.l_slot = self.u_slot = up(st["slot"])
             self.len_l = self.len_u = max(int(st["len"]), 1)
             self.rhs_l = D.zeros(self.len_l)
             self.rhs_u = self.rhs_l

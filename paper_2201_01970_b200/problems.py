@@ -170,50 +170,96 @@ def _assemble(g: _Grid, perm, conv_scale, couple, drift) -> BlockCsrMatrix:
     return BlockCsrMatrix(3, n, n, g.ptr, g.cols, vals)
 
 
-def _rhs(A: BlockCsrMatrix, xs: np.ndarray) -> np.ndarray:
-    """b = A x* for input generation: on the B200 when one is present (the
-    bit-exact device SpMV; the matrix stays resident for the solve that
-    follows), else on the host in the same order."""
+def _cuda_ok() -> bool:
     try:
         import torch
-        if torch.cuda.is_available():
-            from . import device as D
-            return _rhs_device(A, xs)
+        if not torch.cuda.is_available():
+            return False
+        from . import _native as N
+        N.lib()
+        return True
     except (ImportError, OSError, RuntimeError):
-        pass
-    return bsr_matvec_reference_order(A, xs)
+        return False
 
 
-def _rhs_device(A: BlockCsrMatrix, xs: np.ndarray) -> np.ndarray:
-    from . import _native as N
-    from . import device as D
-    M = D.device_matrix(A)
-    x = D.upload(np.ascontiguousarray(xs, dtype=np.float64))
-    y = D.empty(A.nrows * A.block_size)
-    N.check(N.lib().cprb_spmv(M.desc_ref(), A.block_size, D.ptr(x), D.ptr(y), None, D.stream()))
-    return y.cpu().numpy()
+class _DeviceAssembler:
+    """Device assembly (csrc/gen.cu) of one grid's Jacobians: row pointers
+    once, then per step the three random fields in, the BSR (int64 columns,
+    3x3 blocks) out -- bitwise the host restatement's values.  The matrix
+    keeps its device copy (packed straight from the device CSR, no upload)
+    for the solve that follows, and b = A x* is the device SpMV."""
+
+    def __init__(self, nx, ny, nz, xs):
+        from . import _native as N
+        from . import device as D
+        t = D.torch()
+        self.dims = (nx, ny, nz)
+        self.n = nx * ny * nz
+        cnt = t.empty(self.n, dtype=t.int64, device="cuda")
+        N.check(N.lib().cprb_gen_row_counts(nx, ny, nz, D.ptr(cnt), D.stream()))
+        self.ptr_d = t.zeros(self.n + 1, dtype=t.int64, device="cuda")
+        t.cumsum(cnt, 0, out=self.ptr_d[1:])
+        self.ptr = self.ptr_d.cpu().numpy()
+        self.nnz = int(self.ptr[-1])
+        self.cols_d = None
+        self.xs_d = D.upload(xs)
+
+    def assemble(self, perm, conv_scale, couple, drift, with_rhs):
+        from . import _native as N
+        from . import device as D
+        t = D.torch()
+        f64 = D.upload
+        perm_d, conv_d, cpl_d = f64(perm), f64(conv_scale), f64(couple)
+        cols_d = t.empty(self.nnz, dtype=t.int64, device="cuda")
+        vals_d = t.empty(self.nnz * 9, dtype=t.float64, device="cuda")
+        N.check(N.lib().cprb_gen_assemble(*self.dims, float(drift), D.ptr(perm_d), D.ptr(conv_d),
+                                          D.ptr(cpl_d), D.ptr(self.ptr_d), D.ptr(cols_d),
+                                          D.ptr(vals_d), D.stream()))
+        if self.cols_d is None:
+            self.cols = cols_d.cpu().numpy()
+            self.cols_d = cols_d
+        A = BlockCsrMatrix(3, self.n, self.n, self.ptr, self.cols,
+                           vals_d.cpu().numpy().reshape(-1, 3, 3))
+        M = D.device_matrix(A, (self.ptr_d, self.cols_d, vals_d))
+        b = None
+        if with_rhs:
+            y = D.empty(3 * self.n)
+            N.check(N.lib().cprb_spmv(M.desc_ref(), 3, D.ptr(self.xs_d), D.ptr(y), None,
+                                      D.stream()))
+            b = y.cpu().numpy()
+        return A, b
 
 
 def generate_blackoil_like_sequence(nx: int, ny: int, nz: int, nsteps: int, drift: float,
                                     seed: int, with_rhs: bool = True) -> ProblemSequence:
     """Deterministic-by-seed sequence of 3x3-block 7-point systems
-    (src/problems.py:74-110)."""
+    (src/problems.py:74-110).
+
+    The random fields and np.exp are drawn on the host exactly as the
+    reference does; with a B200 present the Jacobians are assembled in HBM
+    (csrc/gen.cu, bitwise equal to the host restatement _assemble) and each
+    matrix keeps its device copy for the solve (device.release_device(A)
+    frees it); otherwise the host restatement assembles them."""
     if min(nx, ny, nz) < 1 or nsteps < 1:
         raise ValueError("grid dimensions and nsteps must be >= 1")
     rng = np.random.default_rng(seed)
-    g = _Grid(nx, ny, nz)
-    n = g.n
+    n = nx * ny * nz
     logk = rng.normal(0.0, 1.0, n)
     conv_scale = rng.uniform(0.2, 0.5, n)
     couple = rng.standard_normal((n, 6)) * 0.5
     xs = manufactured_solution(n)
+    dev = _DeviceAssembler(nx, ny, nz, xs) if _cuda_ok() else None
+    g = None if dev is not None else _Grid(nx, ny, nz)
     systems = []
     for step in range(nsteps):
         if step > 0:
             logk = logk + drift * rng.normal(0.0, 1.0, n)
             conv_scale = conv_scale * np.exp(drift * rng.normal(0.0, 1.0, n))
+        if dev is not None:
+            systems.append(dev.assemble(np.exp(logk), conv_scale, couple, drift, with_rhs))
+            continue
         A = _assemble(g, np.exp(logk), conv_scale, couple, drift)
-        systems.append((A, _rhs(A, xs) if with_rhs else None))
+        systems.append((A, bsr_matvec_reference_order(A, xs) if with_rhs else None))
     return ProblemSequence(systems, provenance={"kind": "synthetic", "nx": nx, "ny": ny,
                                                 "nz": nz, "nsteps": nsteps, "drift": drift,
                                                 "seed": seed})

@@ -329,10 +329,37 @@ def make_big():
     (OUT / "c3_v0.json").write_text(json.dumps(out) + "\n")
 
 
+def make_c4_mix():
+    """Config 4 with a reuse/rebuild MIX (src/cpr.py:204-212, :349-382): ten
+    SPE10-shaped (C3 grid) Newton systems with drift 0.05 and mu = 5, where
+    the aging preconditioner crosses mu and forces rebuilds mid-sequence
+    (about 30 minutes of CPU)."""
+    _import_ref()
+    from cprkit.cpr import SolverConfig, ascpr_gmres_sequence
+    from cprkit.problems import generate_blackoil_like_sequence
+    t0 = time.time()
+    seq = generate_blackoil_like_sequence(60, 220, 85, 10, 0.05, 0)
+    tg = time.time() - t0
+    cfg = SolverConfig(theta=0.0, theta_amg=0.0, cycle="v")
+    t0 = time.time()
+    out = ascpr_gmres_sequence(seq.systems, 5, cfg, keep_solutions=True)
+    tsol = time.time() - t0
+    rec = dict(grid=[60, 220, 85], nsteps=10, drift=0.05, seed=0, mu=5,
+               setup_calls=out.setup_calls, rebuilt=[bool(r.rebuilt) for r in out.records],
+               its=[[r.outer, r.inner] for r in out.records],
+               rel=[r.rel_residual for r in out.records],
+               x_norm=[float(np.linalg.norm(r.x)) for r in out.records],
+               x_sample_stride=997, x_sample=[r.x[::997].tolist() for r in out.records],
+               b_digests=[digest(b) for _, b in seq.systems],
+               seconds=dict(generate=tg, sequence=tsol, setup=out.setup_time, solve=out.solve_time))
+    (OUT / "c4_mix.json").write_text(json.dumps(rec) + "\n")
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
     ap.add_argument("--bigk", action="store_true")
+    ap.add_argument("--c4mix", action="store_true")
     ap.add_argument("--skip-small", action="store_true")
     a = ap.parse_args()
     if not a.skip_small:
@@ -341,3 +368,5 @@ if __name__ == "__main__":
         make_big()
     if a.bigk:
         make_big_k()
+    if a.c4mix:
+        make_c4_mix()

@@ -14,7 +14,7 @@ import pytest
 from paper_2201_01970_b200 import _native as N
 
 ROOT = Path(__file__).resolve().parents[1]
-STRUCTS = {"cprb_sell": N.Sell, "cprb_amg_level": N.AmgLevel, "cprb_tail_level": N.TailLevel,
+STRUCTS = {"cprb_sell": N.Sell, "cprb_amg_level": N.AmgLevel,
            "cprb_amg": N.Amg, "cprb_wave": N.Wave, "cprb_stencil": N.Stencil, "cprb_bilu": N.Bilu, "cprb_cpr": N.Cpr}
 
 

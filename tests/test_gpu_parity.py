@@ -221,48 +221,43 @@ def test_vcycle_matches_oracle_with_same_coarse_solve(gpu):
     np.testing.assert_allclose(P.amg_cycle(B.pressure_solver, r), zo, rtol=1e-13, atol=1e-15)
 
 
-@pytest.mark.parametrize("tail_rows", ["600", "300"])
+@pytest.mark.parametrize("tail_rows", ["0", "300", "600", "5000", "100000"])
 def test_vcycle_persistent_tail_bitwise(gpu, monkeypatch, tail_rows):
-    """The shared-memory-resident cluster tail (csrc/amg.cu k_vtail3) runs the
-    same arithmetic as the per-colour kernels: bitwise equal cycles."""
+    """The persistent single-CTA tail (csrc/vtail.cu: shared-memory vectors,
+    TMA-streamed records) runs the launched kernels' arithmetic: bitwise
+    equal cycles with the tail off, starting at a deep level, a middle
+    level, or covering every level that fits."""
     A, _ = _c1()
-    (A2, _), = P.generate_blackoil_like_sequence(16, 12, 10, 1, 0.01, 1).systems
+    (A2, _), = P.generate_blackoil_like_sequence(40, 30, 20, 1, 0.01, 2).systems
     rng = np.random.default_rng(11)
     for M in (A, A2):
         cfg = P.SolverConfig(theta=0.0, theta_amg=0.0, cycle="v")
+        monkeypatch.setenv("CPRB_TAIL_ROWS", "0")
         h0 = P.build_hierarchy(P.pressure_matrix(M), cfg.amg_params())
         r = rng.standard_normal(M.nrows)
         z0 = P.amg_cycle(h0, r)
+        assert h0.device().desc.tail_start == len(h0.levels) - 1
         monkeypatch.setenv("CPRB_TAIL_ROWS", tail_rows)
         h1 = P.build_hierarchy(P.pressure_matrix(M), cfg.amg_params())
         z1 = P.amg_cycle(h1, r)
-        dev1 = h1.device()
-        assert dev1.desc.tail_mode == 3 and dev1.desc.tail_start < len(h1.levels) - 1
+        if tail_rows in ("5000", "100000"):
+            assert h1.device().desc.tail_start < len(h1.levels) - 1
         monkeypatch.delenv("CPRB_TAIL_ROWS")
         assert np.array_equal(z0, z1)
 
 
-@pytest.mark.parametrize("lv_rows", ["9000", "25000"])
-def test_vcycle_one_cta_levels_bitwise(gpu, monkeypatch, lv_rows):
-    """Coarse levels run as one-CTA passes (csrc/amg.cu k_lv_fwd / k_lv_bwd,
-    x in shared memory) with the per-colour kernels' arithmetic: bitwise
-    equal cycles."""
+def test_vcycle_tail_skips_snapshot_levels(gpu, monkeypatch):
+    """theta_amg > 0 levels with intra-colour couplings stay on the launched
+    path; the cycle is unchanged bitwise."""
     A, _ = _c1()
-    (A2, _), = P.generate_blackoil_like_sequence(40, 30, 20, 1, 0.01, 2).systems
-    rng = np.random.default_rng(12)
-    for M in (A, A2):
-        cfg = P.SolverConfig(theta=0.0, theta_amg=0.0, cycle="v")
-        monkeypatch.setenv("CPRB_LV1_ROWS", "0")
-        h0 = P.build_hierarchy(P.pressure_matrix(M), cfg.amg_params())
-        r = rng.standard_normal(M.nrows)
-        z0 = P.amg_cycle(h0, r)
-        assert not any(dl.desc.one_cta for dl in h0.device().levels)
-        monkeypatch.setenv("CPRB_LV1_ROWS", lv_rows)
-        h1 = P.build_hierarchy(P.pressure_matrix(M), cfg.amg_params())
-        z1 = P.amg_cycle(h1, r)
-        assert sum(dl.desc.one_cta for dl in h1.device().levels) >= 2
-        monkeypatch.delenv("CPRB_LV1_ROWS")
-        assert np.array_equal(z0, z1)
+    cfg = P.SolverConfig(theta=0.0, theta_amg=0.08, cycle="v")
+    r = np.random.default_rng(3).standard_normal(A.nrows)
+    monkeypatch.setenv("CPRB_TAIL_ROWS", "0")
+    z0 = P.amg_cycle(P.build_hierarchy(P.pressure_matrix(A), cfg.amg_params()), r)
+    monkeypatch.delenv("CPRB_TAIL_ROWS")
+    monkeypatch.setenv("CPRB_TAIL_ROWS", "100000")
+    z1 = P.amg_cycle(P.build_hierarchy(P.pressure_matrix(A), cfg.amg_params()), r)
+    assert np.array_equal(z0, z1)
 
 
 def test_device_kcycle_bitwise_equals_host_kcycle(gpu):
@@ -526,3 +521,29 @@ def test_spe10_shape_c3_kcycle_against_reference(gpu):
     xs = P.problems.manufactured_solution(60 * 220 * 85)
     err = np.linalg.norm(res.x - xs) / np.linalg.norm(xs)
     assert abs(err - 4.78e-6) <= 0.01e-6
+
+
+@pytest.mark.slow
+def test_c4_sequence_rebuild_mix_against_reference(gpu):
+    """Config 4 with a reuse/rebuild MIX (tests/golden/c4_mix.json, made by
+    the unmodified reference: make_golden.py --c4mix): ten SPE10-shaped
+    Newton systems, drift 0.05, mu = 5.  The aging preconditioner crosses mu
+    mid-sequence, so ascpr_decide must rebuild exactly where the reference
+    did (src/cpr.py:204-212), with the reference's iteration counts, final
+    residuals (1e-8) and solutions (1e-6)."""
+    path = GOLDEN / "c4_mix.json"
+    if not path.exists():
+        pytest.skip("c4_mix fixture not generated")
+    ref = json.loads(path.read_text())
+    seq = P.generate_blackoil_like_sequence(*ref["grid"], ref["nsteps"], ref["drift"], ref["seed"])
+    cfg = P.SolverConfig(theta=0.0, theta_amg=0.0, cycle="v")
+    out = P.ascpr_gmres_sequence(seq.systems, ref["mu"], cfg, keep_solutions=True)
+    assert out.setup_calls == ref["setup_calls"]
+    assert [r.rebuilt for r in out.records] == ref["rebuilt"]
+    assert any(ref["rebuilt"][1:]) and not all(ref["rebuilt"])
+    assert [[r.outer, r.inner] for r in out.records] == ref["its"]
+    np.testing.assert_allclose([r.rel_residual for r in out.records], ref["rel"], rtol=1e-8)
+    st = ref["x_sample_stride"]
+    for r, xs in zip(out.records, ref["x_sample"]):
+        xs = np.asarray(xs)
+        assert np.linalg.norm(r.x[::st] - xs) <= 1e-6 * np.linalg.norm(xs)

@@ -48,27 +48,25 @@ def main():
     }
     import ctypes as C
     from paper_2201_01970_b200 import _native as N
-    if a.what == "tail3tl":
+    if a.what == "vtailtl":
         t = torch
         log = t.zeros(4096, dtype=t.int64, device="cuda")
-        N.lib().cprb_tail3_set_log(D.ptr(log))
+        N.lib().cprb_vtail_set_log(D.ptr(log))
         for rep in range(3):
             log.zero_()
             N.check(N.lib().cprb_amg_cycle(C.byref(Bd.amg.desc), D.ptr(bd), D.ptr(zp), D.stream()))
             t.cuda.synchronize()
-        N.lib().cprb_tail3_set_log(None)
-        L = log.cpu().numpy()
-        L = L[L > 0]
-        print("mode", Bd.amg.desc.tail_mode, "tail_start", Bd.amg.desc.tail_start,
-              "max bytes", Bd.amg.desc.tail3_max_bytes)
-        if L.size == 0:
-            return
-        d = np.diff(L) / 1e3
-        ph = Bd.amg.tail_phase_list
-        print("tail3 phases", len(d), "total us", (L[-1] - L[0]) / 1e3, "mode", Bd.amg.desc.tail_mode)
-        print("first (load+sync)", d[0] if len(d) else None)
-        for i, (p_, v) in enumerate(zip(ph, d[1:])):
-            print(f"  {i:3d} {p_} {v:.2f}")
+        N.lib().cprb_vtail_set_log(None)
+        d = Bd.amg.desc
+        L = log.cpu().numpy()[:2 + d.tail_nphases]
+        ph = Bd.amg.tail_phase_host
+        print("tail_start", d.tail_start, "phases", d.tail_nphases, "chunks", d.tail_nchunks,
+              "slot", d.tail_slot, "stream bytes", Bd.amg.tail_bytes)
+        print(f"pdl wait {(L[1] - L[0]) / 1e3:.2f} us, total after wait {(L[-1] - L[1]) / 1e3:.2f} us")
+        prev = L[1]
+        for i in range(d.tail_nphases):
+            print(f"  {i:3d} {tuple(int(v) for v in ph[i])} {(L[2 + i] - prev) / 1e3:7.2f} us")
+            prev = L[2 + i]
         return
     if a.what == "amgtl":
         t = torch
