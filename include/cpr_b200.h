@@ -91,6 +91,19 @@ int cprb_lower_level_schedule(int64_t n, const int64_t* ptr, const int64_t* cols
  * in-range neighbours of a natural-ordered grid (nx, ny, nz >= 2), else 0. */
 int cprb_detect_stencil(int64_t n, const int64_t* ptr, const int64_t* cols, int64_t* dims);
 
+/* src/mmio.py:36-95  body of a MatrixMarket coordinate file (after the
+ * header line).  info[12] out: nrows, ncols, nnz, block_size sidecar (-1 =
+ * none), entries read, error code (0 ok; 1 sidecar, 2/3 size line, 4 no size
+ * line, 5 entry, 6 index range (info[7..8] = i, j), 7 too many entries,
+ * 8 count mismatch, 9 token outside the fast grammar), error line, -, -,
+ * total lines.  rows/cols/vals/linenos (capacity nnz) may be NULL to read
+ * the size line only.  Entries are 0-based. */
+int cprb_mm_read_coord(const char* path, int64_t* rows, int64_t* cols, double* vals,
+                       int64_t* linenos, int64_t* info);
+/* src/mmio.py:149-160  append "i j v" lines (1-based, %.17g). */
+int cprb_mm_write_entries(const char* path, int64_t n, const int64_t* rows, const int64_t* cols,
+                          const double* vals);
+
 /* coarsest level (replaces scipy lu_factor/lu_solve, src/amg.py:170-173,
  * :248-249): dense inverse via LU with partial pivoting; a: n*n row-major. */
 int cprb_dense_inverse(int64_t n, const double* a, double* inv);

@@ -28,7 +28,8 @@ from .cpr import (
     gmres_solve,
     pressure_matrix,
 )
-from .problems import ProblemSequence, generate_blackoil_like_sequence
+from .problems import ProblemSequence, generate_blackoil_like_sequence, load_sequence, save_sequence
+from . import mmio
 
 __version__ = "0.1.0"
 
@@ -41,5 +42,5 @@ __all__ = [
     "AscprCache", "CprPreconditioner", "GmresParams", "GmresResult", "SolverConfig",
     "apply_cpr", "ascpr_decide", "ascpr_gmres_sequence", "build_cpr", "fingerprint_of",
     "gmres_solve", "pressure_matrix",
-    "ProblemSequence", "generate_blackoil_like_sequence",
+    "ProblemSequence", "generate_blackoil_like_sequence", "save_sequence", "load_sequence", "mmio",
 ]

@@ -103,6 +103,8 @@ _SIGS = {
     "cprb_stencil_pack": (C.c_int, [C.c_int64, C.c_int32, C.c_int32, C.c_int32, vp, vp, vp, vp,
                                     vp, vp, vp, vp, vp]),
     "cprb_vtail_set_log": (C.c_int, [vp]),
+    "cprb_mm_read_coord": (C.c_int, [C.c_char_p, vp, vp, vp, vp, vp]),
+    "cprb_mm_write_entries": (C.c_int, [C.c_char_p, C.c_int64, vp, vp, vp]),
     "cprb_gen_row_counts": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, vp, vp]),
     "cprb_gen_assemble": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_double, vp, vp, vp, vp,
                                     vp, vp, vp]),

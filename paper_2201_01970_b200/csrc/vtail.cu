@@ -27,7 +27,7 @@
 
 namespace cprb {
 
-constexpr int VT_CONSUMER_WARPS = 16;
+constexpr int VT_CONSUMER_WARPS = 8;
 constexpr int VT_THREADS = 32 * (VT_CONSUMER_WARPS + 1);
 constexpr int VT_NSLOT = 4;
 enum { VT_SWEEP = 1, VT_RR = 3, VT_COARSE = 4, VT_PROLONG = 5 };
@@ -130,23 +130,31 @@ struct VtArgs {
 
 constexpr int VT_NCT = VT_CONSUMER_WARPS * 32;
 
+// the launch's dynamic shared memory, addressed by OFFSETS from this symbol
+// so that every access compiles to LDS/STS (pointers carried through
+// integer address arithmetic otherwise degrade to generic loads)
+extern __shared__ __align__(128) uint8_t vt_smem[];
+
 // one chunk of phase ph (all consumer threads)
-__device__ __forceinline__ void vt_chunk(const int4 ph, const uint8_t* rec, double* vec,
-                                         const int* svec, int nl, int tid) {
+__device__ __forceinline__ void vt_chunk(const int4 ph, uint32_t rec_off, const int* svec, int nl,
+                                         int tid) {
+  double* vec = reinterpret_cast<double*>(vt_smem);
   const int warp = tid >> 5, lane = tid & 31;
-  const int4 hdr = *reinterpret_cast<const int4*>(rec);
+  const int4 hdr = *reinterpret_cast<const int4*>(vt_smem + rec_off);
   const int cnt = hdr.x, W = hdr.y, first = hdr.z;
-  const uint8_t* body = rec + 16;
+  const uint32_t o = rec_off + 16;
+  auto A16 = [](uint32_t v) -> uint32_t { return (v + 15u) & ~15u; };
   const int l = ph.y;
   if (ph.x == VT_SWEEP) {
     double* x = vec + svec[2 * l + 1];
     const double* b = vec + svec[2 * l];
-    const int* lens = reinterpret_cast<const int*>(body);
-    const double* diag = reinterpret_cast<const double*>(al16(body + 4 * cnt));
-    const uint16_t* cols =
-        reinterpret_cast<const uint16_t*>(al16(reinterpret_cast<const uint8_t*>(diag + cnt)));
-    const double* vals =
-        reinterpret_cast<const double*>(al16(reinterpret_cast<const uint8_t*>(cols + (size_t)W * cnt)));
+    const uint32_t o_diag = A16(o + 4u * cnt);
+    const uint32_t o_cols = A16(o_diag + 8u * cnt);
+    const uint32_t o_vals = A16(o_cols + 2u * W * cnt);
+    const int* lens = reinterpret_cast<const int*>(vt_smem + o);
+    const double* diag = reinterpret_cast<const double*>(vt_smem + o_diag);
+    const uint16_t* cols = reinterpret_cast<const uint16_t*>(vt_smem + o_cols);
+    const double* vals = reinterpret_cast<const double*>(vt_smem + o_vals);
     for (int t = tid; t < cnt; t += VT_NCT) {
       const double acc = vt_gsrow(cols, vals, cnt, t, lens[t], x);
       x[first + t] = (b[first + t] - acc) / diag[t];
@@ -155,13 +163,15 @@ __device__ __forceinline__ void vt_chunk(const int4 ph, const uint8_t* rec, doub
     const double* x = vec + svec[2 * l + 1];
     const double* b = vec + svec[2 * l];
     double* bc = vec + svec[2 * (l + 1)];
-    const int* rows = reinterpret_cast<const int*>(body);
-    const int* lens = reinterpret_cast<const int*>(al16(body + 4 * cnt));
-    const int* outs = reinterpret_cast<const int*>(al16(reinterpret_cast<const uint8_t*>(lens + cnt)));
-    const uint16_t* cols =
-        reinterpret_cast<const uint16_t*>(al16(reinterpret_cast<const uint8_t*>(outs + cnt / 2)));
-    const double* vals =
-        reinterpret_cast<const double*>(al16(reinterpret_cast<const uint8_t*>(cols + (size_t)W * cnt)));
+    const uint32_t o_lens = A16(o + 4u * cnt);
+    const uint32_t o_outs = A16(o_lens + 4u * cnt);
+    const uint32_t o_cols = A16(o_outs + 4u * (cnt / 2));
+    const uint32_t o_vals = A16(o_cols + 2u * W * cnt);
+    const int* rows = reinterpret_cast<const int*>(vt_smem + o);
+    const int* lens = reinterpret_cast<const int*>(vt_smem + o_lens);
+    const int* outs = reinterpret_cast<const int*>(vt_smem + o_outs);
+    const uint16_t* cols = reinterpret_cast<const uint16_t*>(vt_smem + o_cols);
+    const double* vals = reinterpret_cast<const double*>(vt_smem + o_vals);
     for (int t0 = 0; t0 < cnt; t0 += VT_NCT) {  // lanes 2I, 2I+1 are neighbours in a warp
       const int t = t0 + tid;
       double res = 0.0;
@@ -178,12 +188,12 @@ __device__ __forceinline__ void vt_chunk(const int4 ph, const uint8_t* rec, doub
   } else if (ph.x == VT_PROLONG) {
     double* x = vec + svec[2 * l + 1];
     const double* xc = vec + svec[2 * (l + 1) + 1];
-    const int* aggp = reinterpret_cast<const int*>(body);
+    const int* aggp = reinterpret_cast<const int*>(vt_smem + o);
     for (int t = tid; t < cnt; t += VT_NCT) x[first + t] = x[first + t] + xc[aggp[t]];
   } else {  // VT_COARSE: rows of inv(A_L) times the coarse b (k_dense_mv order)
     const double* cb = vec + svec[2 * (nl - 1)];
     double* cx = vec + svec[2 * (nl - 1) + 1];
-    const double* rowsd = reinterpret_cast<const double*>(body);
+    const double* rowsd = reinterpret_cast<const double*>(vt_smem + o);
     for (int r = warp; r < cnt; r += VT_CONSUMER_WARPS) {
       const double* row = rowsd + (size_t)r * W;
       double sacc = 0.0;
@@ -225,13 +235,13 @@ __device__ __forceinline__ void vt_epilogue(const VtArgs& a, const double* vec, 
 // per chunk) -- many small requests in flight instead of one bulk copy.
 template <int MODE>
 __global__ void __launch_bounds__(VT_THREADS, 1) k_vtail(const VtArgs a) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  double* vec = reinterpret_cast<double*>(smem);
-  const uint32_t ring = smem_u32(smem) + (uint32_t)(((a.vec_len * 8) + 127) & ~127);
-  const uint32_t bars = ring + (uint32_t)(VT_NSLOT * a.slot);
+  double* vec = reinterpret_cast<double*>(vt_smem);
+  const uint32_t ring_off = (uint32_t)(((a.vec_len * 8) + 127) & ~127);
+  const uint32_t bars_off = ring_off + (uint32_t)(VT_NSLOT * a.slot);
+  const uint32_t ring = smem_u32(vt_smem) + ring_off;
+  const uint32_t bars = smem_u32(vt_smem) + bars_off;
   const uint32_t b_full = bars, b_empty = bars + 8u * VT_NSLOT;
-  uint8_t* ring_g = smem + (ring - smem_u32(smem));
-  int4* sph = reinterpret_cast<int4*>(smem + (bars - smem_u32(smem)) + 8 * 2 * VT_NSLOT);
+  int4* sph = reinterpret_cast<int4*>(vt_smem + bars_off + 8 * 2 * VT_NSLOT);
   int* svec = reinterpret_cast<int*>(sph + a.nphases + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   unsigned long long* const tlog = g_vtail_log;
@@ -267,8 +277,11 @@ __global__ void __launch_bounds__(VT_THREADS, 1) k_vtail(const VtArgs a) {
       const int c1 = sph[p + 1].w;
       for (; c < c1; ++c) {
         const uint32_t s = (uint32_t)(c % VT_NSLOT);
+        if (tlog && tid == 0) tlog[2 + a.nphases + 3 * c] = vt_now();
         mbar_wait(b_full + 8u * s, (uint32_t)(c / VT_NSLOT) & 1u);
-        vt_chunk(ph, ring_g + s * (uint32_t)a.slot, vec, svec, a.nl, tid);
+        if (tlog && tid == 0) tlog[3 + a.nphases + 3 * c] = vt_now();
+        vt_chunk(ph, ring_off + s * (uint32_t)a.slot, svec, a.nl, tid);
+        if (tlog && tid == 0) tlog[4 + a.nphases + 3 * c] = vt_now();
         __syncwarp();
         if (lane == 0) mbar_arrive(b_empty + 8u * s);
       }
@@ -306,7 +319,7 @@ __global__ void __launch_bounds__(VT_THREADS, 1) k_vtail(const VtArgs a) {
         asm volatile("cp.async.wait_group 1;" ::: "memory");
         vt_bar();  // chunk c visible to all; everyone is done with chunk c - 1
         issue(c + 2);
-        vt_chunk(ph, ring_g + (uint32_t)(c % NB) * (uint32_t)a.slot, vec, svec, a.nl, tid);
+        vt_chunk(ph, ring_off + (uint32_t)(c % NB) * (uint32_t)a.slot, svec, a.nl, tid);
       }
       if (tlog && tid == 0) tlog[2 + p] = vt_now();
     }

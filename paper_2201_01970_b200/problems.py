@@ -14,14 +14,16 @@ The right-hand side b = A x* uses the reference's row-sum order
 
 from __future__ import annotations
 
+import json
 from dataclasses import dataclass, field
+from pathlib import Path
 
 import numpy as np
 
 from .sparse import BlockCsrMatrix, CsrMatrix
 
 __all__ = ["ProblemSequence", "generate_blackoil_like_sequence", "poisson_2d",
-           "pressure_operator", "manufactured_solution"]
+           "pressure_operator", "manufactured_solution", "save_sequence", "load_sequence"]
 
 
 @dataclass
@@ -290,3 +292,42 @@ def poisson_2d(nx: int, ny: int) -> CsrMatrix:
         vals.append(np.full(int(m.sum()), -1.0))
     return CsrMatrix.from_coo(np.concatenate(rows), np.concatenate(cols), np.concatenate(vals),
                               (n, n))
+
+
+def save_sequence(seq: ProblemSequence, out_dir) -> Path:
+    """Matrices and right-hand sides as MatrixMarket files plus manifest.json
+    (src/problems.py:158-177); returns the manifest path."""
+    from .mmio import write_block_matrix_market, write_matrix_market, write_vector
+    out = Path(out_dir)
+    out.mkdir(parents=True, exist_ok=True)
+    entries = []
+    for k, (A, rhs) in enumerate(seq.systems, start=1):
+        mpath = out / f"system_{k:03d}.mtx"
+        vpath = out / f"rhs_{k:03d}.mtx"
+        if isinstance(A, BlockCsrMatrix):
+            write_block_matrix_market(mpath, A)
+            bs = A.block_size
+        else:
+            write_matrix_market(mpath, A)
+            bs = 1
+        write_vector(vpath, rhs)
+        entries.append({"matrix": mpath.name, "rhs": vpath.name, "block_size": bs})
+    manifest = {"systems": entries, "provenance": seq.provenance}
+    mpath = out / "manifest.json"
+    mpath.write_text(json.dumps(manifest, indent=2) + "\n")
+    return mpath
+
+
+def load_sequence(manifest_path) -> ProblemSequence:
+    """Recorded Jacobian sequence from a manifest (src/problems.py:180-194)."""
+    from .mmio import read_block_matrix_market, read_matrix_market, read_vector
+    manifest_path = Path(manifest_path)
+    manifest = json.loads(manifest_path.read_text())
+    base = manifest_path.parent
+    systems = []
+    for entry in manifest["systems"]:
+        path = base / entry["matrix"]
+        A = (read_block_matrix_market(path) if entry.get("block_size", 1) > 1
+             else read_matrix_market(path))
+        systems.append((A, read_vector(base / entry["rhs"])))
+    return ProblemSequence(systems, provenance=manifest.get("provenance", {}))

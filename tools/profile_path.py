@@ -67,6 +67,15 @@ def main():
         for i in range(d.tail_nphases):
             print(f"  {i:3d} {tuple(int(v) for v in ph[i])} {(L[2 + i] - prev) / 1e3:7.2f} us")
             prev = L[2 + i]
+        C3 = log.cpu().numpy()[2 + d.tail_nphases:2 + d.tail_nphases + 3 * d.tail_nchunks].reshape(-1, 3)
+        if C3[:, 0].all():
+            w = (C3[:, 1] - C3[:, 0]) / 1e3
+            cpt = (C3[:, 2] - C3[:, 1]) / 1e3
+            gap = (C3[1:, 0] - C3[:-1, 2]) / 1e3
+            print(f"chunks: wait total {w.sum():.1f} us, compute total {cpt.sum():.1f} us, "
+                  f"between-chunk (arrive/barrier/loop) total {gap.sum():.1f} us")
+            for c in range(min(40, len(w))):
+                print(f"   chunk {c:3d} wait {w[c]:6.2f} compute {cpt[c]:6.2f}")
         return
     if a.what == "amgtl":
         t = torch
