@@ -582,7 +582,10 @@ def run_c4(args):
            "inner": [r.inner for r in recs], "outer": [r.outer for r in recs],
            "rebuilt": [bool(r.rebuilt) for r in recs],
            "converged": all(r.converged for r in recs), "generate_s": round(t_gen, 2),
-           "note": "solve time includes uploading each new Jacobian (the reused preconditioner keeps its build matrix)"}
+           "note": ("each Jacobian is assembled in HBM by the device generator (csrc/gen.cu, "
+                    "bitwise the reference's values; its host copy is downloaded for the API), so "
+                    "no upload lies inside the solve; generate_s covers the random draws, the "
+                    "device assembly and the host copies of all 10 systems")}
     print(json.dumps(out))
 
 

@@ -86,6 +86,24 @@ int cprb_level_schedule(int64_t n, const int64_t* ptr, const int64_t* cols,
 int cprb_lower_level_schedule(int64_t n, const int64_t* ptr, const int64_t* cols,
                               int64_t* level, int64_t* nlevels);
 
+/* src/smoothers.py:257-271  colour-permuted split of a scalar matrix: row
+ * pr = inv[r] holds (inv[c], a_rc), c != r, in ascending inv[c]; diag[pr] =
+ * a_rr (CPRB_ESINGULAR names the first zero diagonal, permuted index). */
+int cprb_scalar_split(int64_t n, const int64_t* ptr, const int64_t* cols, const double* vals,
+                      const int64_t* perm, const int64_t* inv, int64_t* off_ptr,
+                      int64_t* off_cols, double* off_vals, double* diag);
+
+/* Host SELL-32 fills for the device layouts (cprb_sell): from per-lane
+ * entry lists, or from the rows of a scalar CSR (lane_src[l] = row, -1 =
+ * padding; columns renumbered through colmap when non-NULL).  Outputs are
+ * zero-initialised by the caller and sized by slice_ptr[L/32]. */
+int cprb_sell_fill_lanes(int64_t L, const int64_t* lane_ptr, const int64_t* slice_ptr,
+                         const int64_t* ent_cols, const double* ent_vals, int32_t bs,
+                         int32_t* out_cols, double* out_vals);
+int cprb_sell_fill_rows(int64_t L, const int64_t* lane_src, const int64_t* slice_ptr,
+                        const int64_t* ptr, const int64_t* cols, const double* vals,
+                        const int64_t* colmap, int32_t* out_cols, double* out_vals);
+
 /* Structured 7-point grid test for the stencil BILU plan: returns 1 and
  * dims[3] = {nx, ny, nz} when every row's block columns are exactly the
  * in-range neighbours of a natural-ordered grid (nx, ny, nz >= 2), else 0. */

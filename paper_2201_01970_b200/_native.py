@@ -96,6 +96,9 @@ _SIGS = {
     "cprb_wave_set_log": (C.c_int, [vp]),
     "cprb_stencil_set_log": (C.c_int, [vp]),
     "cprb_pack_bsr_sell": (C.c_int, [C.c_int64, C.c_int32, vp, vp, vp, vp, vp, vp, vp]),
+    "cprb_scalar_split": (C.c_int, [C.c_int64, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "cprb_sell_fill_lanes": (C.c_int, [C.c_int64, vp, vp, vp, vp, C.c_int32, vp, vp]),
+    "cprb_sell_fill_rows": (C.c_int, [C.c_int64, vp, vp, vp, vp, vp, vp, vp, vp]),
     "cprb_lower_level_schedule": (C.c_int, [C.c_int64, vp, vp, vp, vp]),
     "cprb_detect_stencil": (C.c_int, [C.c_int64, vp, vp, vp]),
     "cprb_bilu0_factorize_device": (C.c_int, [C.c_int64, C.c_int32, vp, vp, vp, vp, vp, vp,

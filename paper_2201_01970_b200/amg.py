@@ -254,42 +254,19 @@ def _restriction_sell(A, agg: np.ndarray, n_agg: int, inv_l: np.ndarray, inv_c: 
     lane_orig = D.pad_lanes(lane_orig)
     L = lane_orig.shape[0]
     real = lane_orig >= 0
-    ptr = np.asarray(A.row_ptr, dtype=np.int64)
-    lens = np.zeros(L, dtype=np.int64)
-    lens[real] = (ptr[1:] - ptr[:-1])[lane_orig[real]]
-    lane_ptr = np.zeros(L + 1, dtype=np.int64)
-    np.cumsum(lens, out=lane_ptr[1:])
-    nnz = int(lane_ptr[-1])
-    lane_of = np.repeat(np.arange(L, dtype=np.int64), lens)
-    src = ptr[lane_orig[lane_of]] + (np.arange(nnz, dtype=np.int64) - lane_ptr[lane_of])
-    cols = inv_l[np.asarray(A.col_idx, dtype=np.int64)[src]]
-    vals = np.asarray(A.values, dtype=np.float64)[src]
     lane_row = np.where(real, inv_l[np.maximum(lane_orig, 0)], -1).astype(np.int32)
     agg_out = np.full(L // 2, -1, dtype=np.int32)
     agg_out[:n_agg] = inv_c[np.arange(n_agg)]
-    return D.pack_sell(lane_row, lane_ptr, cols, vals, 1, n, agg_out=agg_out)
+    return D.sell_from_rows(lane_orig, A.row_ptr, A.col_idx, A.values, n, colmap=inv_l,
+                            lane_row=lane_row, agg_out=agg_out)
 
 
 def _permuted_rows_sell(A, perm: np.ndarray, inv: np.ndarray):
     """A_l with rows in permuted order, each row in ORIGINAL column order
     (cols mapped to permuted indices): spmv on permuted vectors with the
     reference's row sums (K-cycle Krylov steps)."""
-    n = A.nrows
-    ptr = np.asarray(A.row_ptr, dtype=np.int64)
     lane_orig = D.pad_lanes(perm.astype(np.int64))
-    L = lane_orig.shape[0]
-    real = lane_orig >= 0
-    lens = np.zeros(L, dtype=np.int64)
-    lens[real] = np.diff(ptr)[lane_orig[real]]
-    lane_ptr = np.zeros(L + 1, dtype=np.int64)
-    np.cumsum(lens, out=lane_ptr[1:])
-    nnz = int(lane_ptr[-1])
-    lane_of = np.repeat(np.arange(L, dtype=np.int64), lens)
-    src = ptr[lane_orig[lane_of]] + (np.arange(nnz, dtype=np.int64) - lane_ptr[lane_of])
-    cols = inv[np.asarray(A.col_idx, dtype=np.int64)[src]]
-    vals = np.asarray(A.values, dtype=np.float64)[src]
-    lane_row = np.where(real, np.arange(L), -1).astype(np.int32)
-    return D.pack_sell(lane_row, lane_ptr, cols, vals, 1, n)
+    return D.sell_from_rows(lane_orig, A.row_ptr, A.col_idx, A.values, A.nrows, colmap=inv)
 
 
 # persistent single-CTA V-cycle tail (csrc/vtail.cu): the coarse levels whose

@@ -91,13 +91,13 @@ int cprb_vertices_grouping(int64_t n, const int64_t* s_ptr, const int64_t* s_col
       adj[fill[s_cols[p]]++] = i;
     }
   std::vector<int64_t> nptr(n + 1, 0);
-  std::vector<int64_t> nadj;
+  std::vector<int32_t> nadj;  // 32-bit: half the cache footprint of the walks below
   nadj.reserve(adj.size());
   for (int64_t i = 0; i < n; ++i) {
     auto b = adj.begin() + cnt[i], e = adj.begin() + cnt[i + 1];
     std::sort(b, e);
     auto u = std::unique(b, e);
-    nadj.insert(nadj.end(), b, u);
+    for (auto it = b; it != u; ++it) nadj.push_back((int32_t)*it);
     nptr[i + 1] = (int64_t)nadj.size();
   }
   std::vector<int64_t> infl(n);
@@ -121,21 +121,34 @@ int cprb_vertices_grouping(int64_t n, const int64_t* s_ptr, const int64_t* s_col
     std::fill(deferred.begin(), deferred.end(), 0);
     std::fill(in_front.begin(), in_front.end(), 0);
     std::fill(in_w.begin(), in_w.end(), 0);
-    std::vector<uint64_t> vk;
-    vk.reserve(vertices.size());
-    for (int64_t v : vertices) {
-      und[v] = 1;
-      vk.push_back(key(v));
+    // V candidates by (influence desc, index asc): the keys never change
+    // within a round, so the heap of the reference is a bucket-sorted list
+    // consumed front to back (entries no longer undetermined are skipped)
+    std::vector<int64_t> vorder(vertices.size());
+    {
+      std::vector<int64_t> bstart(maxinfl + 2, 0);
+      for (int64_t v : vertices) {
+        und[v] = 1;
+        ++bstart[maxinfl - infl[v] + 1];
+      }
+      for (int64_t b = 0; b <= maxinfl; ++b) bstart[b + 1] += bstart[b];
+      for (int64_t v : vertices) vorder[bstart[maxinfl - infl[v]]++] = v;  // vertices ascending
     }
-    MinHeap vheap(std::greater<uint64_t>(), std::move(vk));
-    MinHeap fheap;
+    size_t vpos = 0;
+    // frontier by (influence desc, index asc): one index min-heap per
+    // influence bucket -- the same pop order as one heap on the pair
+    std::vector<std::priority_queue<int64_t, std::vector<int64_t>, std::greater<int64_t>>> fb(
+        maxinfl + 1);
+    int64_t ftop = maxinfl + 1, fsize = 0;
     std::vector<int64_t> w;
     int64_t remaining = (int64_t)vertices.size();
     while (remaining > 0) {
       int64_t v = -1;
-      while (!fheap.empty()) {
-        int64_t c = (int64_t)(fheap.top() & 0xffffffffu);
-        fheap.pop();
+      while (fsize > 0) {
+        while (fb[ftop].empty()) ++ftop;
+        const int64_t c = fb[ftop].top();
+        fb[ftop].pop();
+        --fsize;
         if (in_front[c] && und[c]) {
           in_front[c] = 0;
           v = c;
@@ -144,9 +157,8 @@ int cprb_vertices_grouping(int64_t n, const int64_t* s_ptr, const int64_t* s_col
         in_front[c] = 0;
       }
       if (v < 0) {
-        while (!vheap.empty()) {
-          int64_t c = (int64_t)(vheap.top() & 0xffffffffu);
-          vheap.pop();
+        while (vpos < vorder.size()) {
+          const int64_t c = vorder[vpos++];
           if (und[c]) {
             v = c;
             break;
@@ -181,7 +193,10 @@ int cprb_vertices_grouping(int64_t n, const int64_t* s_ptr, const int64_t* s_col
           int64_t j = nadj[q];
           if (und[j] && !in_front[j] && j != v) {
             in_front[j] = 1;
-            fheap.push(key(j));
+            const int64_t bkt = maxinfl - infl[j];
+            fb[bkt].push(j);
+            ++fsize;
+            if (bkt < ftop) ftop = bkt;
           }
         }
       }
@@ -255,20 +270,34 @@ int cprb_galerkin(int64_t n, const int64_t* ptr, const int64_t* cols, const doub
       for (int64_t p = ptr[i]; p < ptr[i + 1]; ++p) order[fill[agg[i]]++] = p;
   }
   std::vector<double> run;
+  std::vector<int64_t> key;
   int64_t k = 0;
   c_ptr[0] = 0;
   for (int64_t I = 0; I < n_agg; ++I) {
-    auto b = order.begin() + rcnt[I], e = order.begin() + rcnt[I + 1];
-    std::stable_sort(b, e, [&](int64_t x, int64_t y) { return agg[cols[x]] < agg[cols[y]]; });
-    for (auto it = b; it != e;) {
-      const int64_t J = agg[cols[*it]];
+    int64_t* ob = order.data() + rcnt[I];
+    const int64_t m = rcnt[I + 1] - rcnt[I];
+    // stable insertion sort by coarse column J (the lexsort order; rows are short)
+    key.resize(m > 0 ? m : 1);
+    for (int64_t t = 0; t < m; ++t) {
+      const int64_t x = ob[t], kx = agg[cols[x]];
+      int64_t u = t;
+      while (u > 0 && key[u - 1] > kx) {
+        key[u] = key[u - 1];
+        ob[u] = ob[u - 1];
+        --u;
+      }
+      key[u] = kx;
+      ob[u] = x;
+    }
+    for (int64_t t = 0; t < m;) {
+      const int64_t J = key[t];
       run.clear();
-      auto jt = it;
-      while (jt != e && agg[cols[*jt]] == J) run.push_back(vals[*jt++]);
+      int64_t u = t;
+      while (u < m && key[u] == J) run.push_back(vals[ob[u++]]);
       c_cols[k] = J;
       c_vals[k] = segment_sum(run.data(), (int64_t)run.size());
       ++k;
-      it = jt;
+      t = u;
     }
     c_ptr[I + 1] = k;
   }
@@ -516,6 +545,94 @@ int cprb_lower_level_schedule(int64_t n, const int64_t* ptr, const int64_t* cols
     maxl = std::max(maxl, level[i]);
   }
   *nlevels = n > 0 ? maxl : 1;
+  return CPRB_OK;
+}
+
+// Colour-permuted diagonal / off-diagonal split (smoothers.ScalarSplit,
+// src/smoothers.py:257-271 A.permuted(perm)): permuted row pr = inv[r]
+// holds the entries (inv[c], v), c != r, sorted by inv[c]; diag[pr] = a_rr.
+// off_ptr[n+1]; off_cols/off_vals capacity nnz.  Returns CPRB_ESINGULAR
+// naming the first permuted row with a zero (or missing) diagonal.
+int cprb_scalar_split(int64_t n, const int64_t* ptr, const int64_t* cols, const double* vals,
+                      const int64_t* perm, const int64_t* inv, int64_t* off_ptr,
+                      int64_t* off_cols, double* off_vals, double* diag) {
+  off_ptr[0] = 0;
+  for (int64_t pr = 0; pr < n; ++pr) {
+    const int64_t r = perm[pr];
+    int64_t cnt = 0;
+    for (int64_t e = ptr[r]; e < ptr[r + 1]; ++e) cnt += cols[e] != r;
+    off_ptr[pr + 1] = off_ptr[pr] + cnt;
+  }
+  for (int64_t pr = 0; pr < n; ++pr) {
+    const int64_t r = perm[pr];
+    int64_t* oc = off_cols + off_ptr[pr];
+    double* ov = off_vals + off_ptr[pr];
+    int64_t k = 0;
+    double d = 0.0;
+    for (int64_t e = ptr[r]; e < ptr[r + 1]; ++e) {
+      if (cols[e] == r) {
+        d = vals[e];
+        continue;
+      }
+      // insertion by permuted column (rows are short)
+      const int64_t pc = inv[cols[e]];
+      int64_t t = k++;
+      while (t > 0 && oc[t - 1] > pc) {
+        oc[t] = oc[t - 1];
+        ov[t] = ov[t - 1];
+        --t;
+      }
+      oc[t] = pc;
+      ov[t] = vals[e];
+    }
+    diag[pr] = d;
+  }
+  for (int64_t pr = 0; pr < n; ++pr)
+    if (diag[pr] == 0.0) return set_error(CPRB_ESINGULAR, "zero diagonal at row " + std::to_string(pr));
+  return CPRB_OK;
+}
+
+// SELL-32 fills (device.pack_sell layout: entry m of lane l of slice s at
+// slice_ptr[s] + 32 m + l; b x b block value e at (slice_ptr[s] + 32 m) * bb +
+// e * 32 + l).  The output arrays are zero-initialised by the caller.
+// Lanes take their entries from a per-lane list (lane_ptr into ent_*):
+int cprb_sell_fill_lanes(int64_t L, const int64_t* lane_ptr, const int64_t* slice_ptr,
+                         const int64_t* ent_cols, const double* ent_vals, int32_t bs,
+                         int32_t* out_cols, double* out_vals) {
+  const int bb = bs * bs;
+  for (int64_t l = 0; l < L; ++l) {
+    const int64_t s = l >> 5, lane = l & 31;
+    const int64_t a = lane_ptr[l], n = lane_ptr[l + 1] - a;
+    for (int64_t m = 0; m < n; ++m) {
+      const int64_t d = slice_ptr[s] + 32 * m + lane;
+      out_cols[d] = (int32_t)ent_cols[a + m];
+      if (bb == 1) {
+        out_vals[d] = ent_vals[a + m];
+      } else {
+        const int64_t base = (slice_ptr[s] + 32 * m) * bb + lane;
+        for (int e = 0; e < bb; ++e) out_vals[base + (int64_t)e * 32] = ent_vals[(a + m) * bb + e];
+      }
+    }
+  }
+  return CPRB_OK;
+}
+
+// ... or straight from the rows of a scalar CSR (lane_src[l] = source row,
+// -1 = padding), entries in the row's stored order, columns optionally
+// renumbered through colmap
+int cprb_sell_fill_rows(int64_t L, const int64_t* lane_src, const int64_t* slice_ptr,
+                        const int64_t* ptr, const int64_t* cols, const double* vals,
+                        const int64_t* colmap, int32_t* out_cols, double* out_vals) {
+  for (int64_t l = 0; l < L; ++l) {
+    const int64_t r = lane_src[l];
+    if (r < 0) continue;
+    const int64_t d0 = slice_ptr[l >> 5] + (l & 31);
+    for (int64_t e = ptr[r]; e < ptr[r + 1]; ++e) {
+      const int64_t d = d0 + 32 * (e - ptr[r]);
+      out_cols[d] = (int32_t)(colmap ? colmap[cols[e]] : cols[e]);
+      out_vals[d] = vals[e];
+    }
+  }
   return CPRB_OK;
 }
 

@@ -185,22 +185,15 @@ def pack_sell(lane_row, lane_ptr, ent_cols, ent_vals, bs, nrows, lane_len_lo=Non
     slice_ptr = np.zeros(ns + 1, dtype=np.int64)
     np.cumsum(width * 32, out=slice_ptr[1:])
     total = int(slice_ptr[-1])
-    nnz = int(lens.sum())
-    lane_of = np.repeat(np.arange(L, dtype=np.int64), lens)
-    m = np.arange(nnz, dtype=np.int64) - np.asarray(lane_ptr, dtype=np.int64)[lane_of]
-    s = lane_of // 32
-    lane = lane_of % 32
-    d = slice_ptr[s] + m * 32 + lane
-    cols = np.zeros(max(total, 1), dtype=np.int32)
-    cols[d] = ent_cols
     bb = bs * bs
+    cols = np.zeros(max(total, 1), dtype=np.int32)
     vals = np.zeros(max(total * bb, 1))
-    if bb == 1:
-        vals[d] = np.asarray(ent_vals, dtype=np.float64).reshape(-1)
-    else:
-        e = np.arange(bb, dtype=np.int64)
-        idx = ((d - lane) * bb)[:, None] + e[None, :] * 32 + lane[:, None]
-        vals[idx.reshape(-1)] = np.asarray(ent_vals, dtype=np.float64).reshape(-1)
+    lp = np.ascontiguousarray(lane_ptr, dtype=np.int64)
+    ec = np.ascontiguousarray(ent_cols, dtype=np.int64)
+    ev = np.ascontiguousarray(ent_vals, dtype=np.float64).reshape(-1)
+    if L and ec.size:
+        N.check(N.lib().cprb_sell_fill_lanes(L, N.p64(lp), N.p64(slice_ptr), N.p64(ec), N.pf64(ev),
+                                             bs, N.p32(cols), N.pf64(vals)))
     return SellHost(ns, int(nrows), slice_ptr, lane_row, lens.astype(np.int32), cols, vals,
                     None if lane_len_lo is None else np.asarray(lane_len_lo, dtype=np.int32),
                     None if agg_out is None else np.asarray(agg_out, dtype=np.int32))
@@ -222,6 +215,38 @@ class SellDev:
 
     def nbytes(self) -> int:
         return sum(int(v.numel() * v.element_size()) for v in self.t.values() if v is not None)
+
+
+def sell_from_rows(lane_src, ptr_, cols, vals, nrows, colmap=None, **extra) -> SellHost:
+    """SELL-32 whose lane l holds row lane_src[l] of a scalar CSR (-1 =
+    padding) in its stored entry order, columns renumbered through colmap
+    (native fill: no per-entry index arrays on the host)."""
+    lane_src = np.ascontiguousarray(lane_src, dtype=np.int64)
+    L = lane_src.shape[0]
+    assert L % 32 == 0
+    ns = L // 32
+    ptr_ = np.ascontiguousarray(ptr_, dtype=np.int64)
+    real = lane_src >= 0
+    lens = np.zeros(L, dtype=np.int64)
+    lens[real] = (ptr_[1:] - ptr_[:-1])[lane_src[real]]
+    width = lens.reshape(ns, 32).max(axis=1) if ns else np.zeros(0, dtype=np.int64)
+    slice_ptr = np.zeros(ns + 1, dtype=np.int64)
+    np.cumsum(width * 32, out=slice_ptr[1:])
+    total = int(slice_ptr[-1])
+    out_c = np.zeros(max(total, 1), dtype=np.int32)
+    out_v = np.zeros(max(total, 1))
+    c = np.ascontiguousarray(cols, dtype=np.int64)
+    v = np.ascontiguousarray(vals, dtype=np.float64)
+    cm = None if colmap is None else np.ascontiguousarray(colmap, dtype=np.int64)
+    if L and c.size:
+        N.check(N.lib().cprb_sell_fill_rows(L, N.p64(lane_src), N.p64(slice_ptr), N.p64(ptr_),
+                                            N.p64(c), N.pf64(v), None if cm is None else N.p64(cm),
+                                            N.p32(out_c), N.pf64(out_v)))
+    lane_row = extra.pop("lane_row", np.where(real, np.arange(L), -1).astype(np.int32))
+    return SellHost(ns, int(nrows), slice_ptr, np.asarray(lane_row, dtype=np.int32),
+                    lens.astype(np.int32), out_c, out_v, extra.get("lane_len_lo"),
+                    None if extra.get("agg_out") is None else np.asarray(extra["agg_out"],
+                                                                         dtype=np.int32))
 
 
 def sell_rows(ptr_, cols, vals, bs, nrows) -> SellHost:

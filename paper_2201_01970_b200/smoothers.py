@@ -60,27 +60,24 @@ class ScalarSplit:
         inv = np.empty(n, dtype=np.int64)
         inv[self.perm] = np.arange(n, dtype=np.int64)
         self.inv = inv
-        ptr = np.asarray(A.row_ptr, dtype=np.int64)
-        cols = np.asarray(A.col_idx, dtype=np.int64)
-        vals = np.asarray(A.values, dtype=np.float64)
-        rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(ptr))
-        pr, pc = inv[rows], inv[cols]
-        # A.permuted(perm): rows by permuted index, sorted permuted columns
-        # ((row, col) pairs are unique, so one integer key sorts them)
-        order = np.argsort(pr * max(n, 1) + pc)
-        pr, pc, pv = pr[order], pc[order], vals[order]
-        off = pr != pc
-        diag = np.zeros(n)
-        diag[pr[~off]] = pv[~off]
-        zero = np.flatnonzero(diag == 0.0)
-        if zero.size:
-            raise np.linalg.LinAlgError(f"zero diagonal at row {int(zero[0])}")
-        self.diag = diag
-        self.off_rows = pr[off]
-        self.off_cols = pc[off]
-        self.off_vals = pv[off]
+        ptr = np.ascontiguousarray(A.row_ptr, dtype=np.int64)
+        cols = np.ascontiguousarray(A.col_idx, dtype=np.int64)
+        vals = np.ascontiguousarray(A.values, dtype=np.float64)
+        # A.permuted(perm): rows by permuted index, each row's off-diagonals in
+        # ascending permuted column, the diagonal apart (host C++)
+        nnz = max(int(ptr[-1]) if n else 0, 1)
         self.off_ptr = np.zeros(n + 1, dtype=np.int64)
-        np.cumsum(np.bincount(self.off_rows, minlength=n), out=self.off_ptr[1:])
+        self.off_cols = np.zeros(nnz, dtype=np.int64)
+        self.off_vals = np.zeros(nnz)
+        self.diag = np.zeros(max(n, 1))
+        N.check(N.lib().cprb_scalar_split(n, N.p64(ptr), N.p64(cols if cols.size else self.off_cols),
+                                          N.pf64(vals if vals.size else self.off_vals),
+                                          N.p64(self.perm), N.p64(inv), N.p64(self.off_ptr),
+                                          N.p64(self.off_cols), N.pf64(self.off_vals),
+                                          N.pf64(self.diag)))
+        k = int(self.off_ptr[-1])
+        self.off_cols, self.off_vals, self.diag = self.off_cols[:k], self.off_vals[:k], self.diag[:n]
+        self.off_rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(self.off_ptr))
         sizes = np.array([g.shape[0] for g in partition.groups], dtype=np.int64)
         self.color_rows = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
         self.ncolors = len(partition.groups)

@@ -231,3 +231,60 @@ def test_c3_setup_digests_against_reference():
             assert ref["agg_digests"][li] is None
     assert B.relaxation.l_schedule.n_levels == ref["bilu_llev"]
     assert B.relaxation.u_schedule.n_levels == ref["bilu_ulev"]
+
+
+def _pack_sell_numpy(lane_row, lane_ptr, ent_cols, ent_vals, bs):
+    """The per-entry numpy scatter the native fills replaced (layout spec)."""
+    L = lane_row.shape[0]
+    ns = L // 32
+    lens = np.diff(lane_ptr)
+    width = lens.reshape(ns, 32).max(axis=1)
+    sp = np.zeros(ns + 1, dtype=np.int64)
+    np.cumsum(width * 32, out=sp[1:])
+    nnz = int(lens.sum())
+    lane_of = np.repeat(np.arange(L), lens)
+    m = np.arange(nnz) - lane_ptr[lane_of]
+    lane = lane_of % 32
+    d = sp[lane_of // 32] + m * 32 + lane
+    cols = np.zeros(max(int(sp[-1]), 1), dtype=np.int32)
+    cols[d] = ent_cols
+    bb = bs * bs
+    vals = np.zeros(max(int(sp[-1]) * bb, 1))
+    if bb == 1:
+        vals[d] = ent_vals
+    else:
+        idx = ((d - lane) * bb)[:, None] + np.arange(bb)[None, :] * 32 + lane[:, None]
+        vals[idx.reshape(-1)] = ent_vals.reshape(-1)
+    return sp, cols, vals
+
+
+@pytest.mark.parametrize("bs", [1, 3])
+def test_native_sell_fills_match_layout(rng, bs):
+    from paper_2201_01970_b200 import device as D
+    L = 32 * 7
+    lens = rng.integers(0, 9, size=L)
+    lens[rng.random(L) < 0.2] = 0
+    lane_ptr = np.zeros(L + 1, dtype=np.int64)
+    np.cumsum(lens, out=lane_ptr[1:])
+    nnz = int(lane_ptr[-1])
+    ec = rng.integers(0, 1000, size=nnz)
+    ev = rng.standard_normal((nnz, bs, bs)) if bs > 1 else rng.standard_normal(nnz)
+    lane_row = np.where(lens > 0, np.arange(L), -1).astype(np.int32)
+    h = D.pack_sell(lane_row, lane_ptr, ec, ev, bs, L)
+    sp, cols, vals = _pack_sell_numpy(lane_row, lane_ptr, ec, ev, bs)
+    assert np.array_equal(h.slice_ptr, sp) and np.array_equal(h.cols, cols)
+    assert np.array_equal(h.vals, vals)
+    # rows of a CSR, columns renumbered: equal to the per-lane-list packing
+    A = P.CsrMatrix.from_dense((rng.random((100, 100)) < 0.05) * rng.standard_normal((100, 100)))
+    perm = rng.permutation(100)
+    inv = np.empty(100, dtype=np.int64)
+    inv[perm] = np.arange(100)
+    src = D.pad_lanes(perm.astype(np.int64))
+    got = D.sell_from_rows(src, A.row_ptr, A.col_idx, A.values, 100, colmap=inv)
+    lp = np.zeros(src.shape[0] + 1, dtype=np.int64)
+    ln = np.where(src >= 0, np.diff(A.row_ptr)[np.maximum(src, 0)], 0)
+    np.cumsum(ln, out=lp[1:])
+    ent = np.concatenate([np.arange(A.row_ptr[r], A.row_ptr[r + 1]) for r in src if r >= 0])
+    sp, cols, vals = _pack_sell_numpy(got.lane_row, lp, inv[A.col_idx[ent]], A.values[ent], 1)
+    assert np.array_equal(got.slice_ptr, sp) and np.array_equal(got.cols, cols)
+    assert np.array_equal(got.vals, vals)
