@@ -10,6 +10,7 @@ entries in the order the reference sums them.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -39,6 +40,9 @@ def stream() -> int:
     return torch().cuda.current_stream().cuda_stream
 
 
+_SETUP_SYNC = os.environ.get("CPRB_SETUP_SYNC", "0") == "1"
+
+
 def bind_current(fn):
     """Wrap fn so that, run on a setup-pool thread, it uses the caller's CUDA
     device and stream (torch keeps both per thread)."""
@@ -48,7 +52,10 @@ def bind_current(fn):
 
     def run(*args, **kw):
         with t.cuda.device(dev), t.cuda.stream(st):
-            return fn(*args, **kw)
+            out = fn(*args, **kw)
+            if _SETUP_SYNC:
+                t.cuda.current_stream().synchronize()
+            return out
     return run
 
 
