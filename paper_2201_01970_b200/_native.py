@@ -8,12 +8,14 @@ import of a device path raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import warnings
 from pathlib import Path
 
 import numpy as np
 
-_LIB_PATH = Path(__file__).resolve().parent / "_native" / "libcprb200.so"
+_LIB_PATH = Path(os.environ.get("CPRB_LIB") or
+                 Path(__file__).resolve().parent / "_native" / "libcprb200.so")
 _lib = None
 
 OK, EINVAL, ENONFINITE, ESINGULAR, EDEVICE, ERUNTIME, EUNSUPPORTED = range(7)

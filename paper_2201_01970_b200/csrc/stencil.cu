@@ -33,6 +33,7 @@
 // identity, so the sum of the present terms is unchanged bit for bit) and
 // 0.0 for a row without neighbours.
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "device.cuh"
 #include "engine.h"
@@ -44,7 +45,9 @@ namespace cg = cooperative_groups;
 namespace cprb {
 
 constexpr int STENCIL_SMEM = 210 * 1024;
-constexpr int STENCIL_CLUSTER = 8;   // planes per thread-block cluster (DSMEM hand-offs)
+#ifndef STENCIL_CLUSTER
+#define STENCIL_CLUSTER 8   // planes per thread-block cluster (DSMEM hand-offs)
+#endif
 constexpr int STENCIL_RZ = 8;        // pushed diagonals in flight per segment
 constexpr int STENCIL_LAG = 8;       // diagonals a cluster's first plane lets its producer lead
 constexpr int STENCIL_DMAX = 1024;   // anti-diagonals per plane (nx + ny - 1) held in smem
@@ -118,12 +121,59 @@ __device__ __forceinline__ void stencil_wait3(const double* g, double* v) {
   int spins = 0;
   while (stencil_is_sentinel(v[0]) || stencil_is_sentinel(v[1]) || stencil_is_sentinel(v[2])) {
     if (++spins > 8) __nanosleep(20);
+#ifdef STENCIL_DIAG
+    if (spins > (1 << 22)) __trap();
+#endif
     if (spins > (1 << 27)) __trap();  // a producer that never publishes: fail, do not hang
 #pragma unroll
     for (int c = 0; c < 3; ++c)
       if (stencil_is_sentinel(v[c])) v[c] = ld_relaxed(g + c);
   }
 }
+
+#ifdef STENCIL_DIAG
+// diagnostic build only (tools/build_variant.py ... -DSTENCIL_DIAG): per-warp
+// progress marks in host-mapped memory and bounded waits that trap
+__device__ int* g_sdiag = nullptr;
+__device__ __forceinline__ void sd_mark(int kr, int t, int m, int x) {
+  if (g_sdiag && blockIdx.x < 512 && (threadIdx.x & 31) == 0) {
+    volatile int* e = g_sdiag + (blockIdx.x * 8 + (threadIdx.x >> 5)) * 8;
+    e[0] = kr;
+    e[1] = t;
+    e[2] = m;
+    e[3] = x;
+  }
+}
+__device__ __forceinline__ void st_wait(uint32_t bar, uint32_t parity) {
+  for (long long k = 0;; ++k) {
+    uint32_t done;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (k == (1ll << 20) && g_sdiag && blockIdx.x < 512) {
+      unsigned long long raw;
+      asm volatile("ld.shared.b64 %0, [%1];" : "=l"(raw) : "r"(bar) : "memory");
+      volatile int* e = g_sdiag + (blockIdx.x * 8 + (threadIdx.x >> 5)) * 8;
+      e[4] = (int)(raw & 0xffffffffu);
+      e[5] = (int)(raw >> 32);
+      e[6] = (int)parity;
+      e[7] = (int)(bar & 0xffff);
+    }
+    if (k > (1ll << 22)) __trap();
+  }
+}
+#define SD_MARK(kr, t, m, x) sd_mark((kr), (t), (m), (int)(x))
+#define ST_WAIT(b, p) st_wait((b), (p))
+#else
+#define SD_MARK(kr, t, m, x) \
+  do {                       \
+  } while (0)
+#define ST_WAIT(b, p) mbar_wait((b), (p))
+#endif
 
 // UPPER = false: z = r - sum_{-z,-y,-x} L z             (rhs = r, out = z)
 // UPPER = true : y = inv(U_ii) (z - sum_{+x,+y,+z} U y)  (rhs = z, out = y)
@@ -162,7 +212,7 @@ __global__ void __launch_bounds__(32 * (S + 1), 1)
       mbar_init(b_empty + 8u * k, S);
     }
     for (int k = 0; k < S * RZ; ++k) {
-      mbar_init(b_zfull + 8u * k, 1);
+      mbar_init(b_zfull + 8u * k, 2);  // the receiver's arming + the sender's arrival
       mbar_init(b_zempty + 8u * k, 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -173,15 +223,23 @@ __global__ void __launch_bounds__(32 * (S + 1), 1)
   unsigned long long* const tlog = TL ? g_stencil_log : nullptr;  // diagnostic variant only
   uint32_t g = 0;   // TMA ring uses (slot g % R, phase (g / R) & 1)
   uint32_t gz = 0;  // pushed / received diagonals (slot gz % RZ, phase (gz / RZ) & 1)
-  // one cluster = C consecutive planes; clusters take them in ticket order
-  // (whichever cluster is scheduled first takes the lowest), so a cluster
-  // only ever waits on one that is already running or finished
-  do {
+  // one round = C consecutive planes, one per rank; rounds are taken in
+  // ticket order.  Persistent clusters: the grid holds only as many clusters as can be
+  // resident at once (launch_stencil_s), and each takes rounds of C planes
+  // until all are done, so a round only waits on an earlier round held by a
+  // running cluster.  (With more clusters than fit, the hardware's placement
+  // of the waiting ones does not follow ticket order: measured to deadlock.)
+  int kr_last = -1;
+  for (;;) {
+    SD_MARK(kr_last, -1, 5, 0);
     if (threadIdx.x == 0 && rank == 0) s_ticket[0] = atomicAdd(ticket, 1);
     cluster.sync();
     const int kround = *cluster.map_shared_rank(s_ticket, 0);
+    cluster.sync();                    // every rank read the ticket before the next one is taken
+    if (kround * C >= nz) break;       // cluster-uniform: no rounds left
+    kr_last = kround;
     const int zt = kround * C + rank;  // plane in processing order
-    if (zt >= nz) break;               // idle rank of the last cluster
+    if (zt >= nz) continue;            // idle rank of the last round
     const int z = UPPER ? nz - 1 - zt : zt;
     const int64_t pbase = (int64_t)z * T.P;
     if (warp == S) {
@@ -191,7 +249,8 @@ __global__ void __launch_bounds__(32 * (S + 1), 1)
           const int d = UPPER ? D - 1 - t : t;
           const int o = s_doff[d], wp = s_doff[d + 1] - o;
           const uint32_t slot = g % (uint32_t)R;
-          if (g >= (uint32_t)R) mbar_wait(b_empty + 8u * slot, ((g / (uint32_t)R) - 1u) & 1u);
+          SD_MARK(kround, t, 6, g);
+          if (g >= (uint32_t)R) ST_WAIT(b_empty + 8u * slot, ((g / (uint32_t)R) - 1u) & 1u);
           const uint32_t bar = b_full + 8u * slot;
           const uint32_t rb = (uint32_t)(NF * 8 * wp), hb = (uint32_t)(24 * wp);
           mbar_expect_tx(bar, rb + hb);
@@ -199,7 +258,8 @@ __global__ void __launch_bounds__(32 * (S + 1), 1)
           bulk_g2s(s_ring + slot * SLOT + REC, rhs + (pbase + o) * 3, hb, bar);
         }
       }
-      break;
+      __syncwarp();  // the warp reaches the next cluster barrier converged
+      continue;
     }
     const int s = warp;
     const int ix = 32 * s + lane;
@@ -241,6 +301,7 @@ __global__ void __launch_bounds__(32 * (S + 1), 1)
       const int d = UPPER ? D - 1 - tl : tl;
       const int lo = d - (ny - 1) > 0 ? d - (ny - 1) : 0;
       const int hi = d < nx - 1 ? d : nx - 1;
+      SD_MARK(kround, -1, 7, 0);
       if (ix >= lo && ix <= hi) {
         double v[3];
         const double* gq = zplane + 3 * (s_doff[d] + ix - lo);
@@ -297,7 +358,8 @@ __global__ void __launch_bounds__(32 * (S + 1), 1)
       if (has_z) {
         long long tz0 = tlog ? clock64() : 0;
         if (z_push) {
-          mbar_wait(my_zfull + 8u * zslot, (gz / (uint32_t)RZ) & 1u);
+          SD_MARK(kround, t, 1, gz);
+          ST_WAIT(my_zfull + 8u * zslot, (gz / (uint32_t)RZ) & 1u);
           if (ok) {
             const uint32_t a = my_zbuf + zslot * 768u + 24u * (uint32_t)(ix - first);
 #pragma unroll
@@ -310,13 +372,15 @@ __global__ void __launch_bounds__(32 * (S + 1), 1)
             zq0[c] = zq1[c];
           }
           zload(t + 2, zq1);
+          SD_MARK(kround, t, 8, 0);
           if (ok) stencil_wait3(zplane + 3 * (o + j), zv);
         }
         if (tlog) c_z += clock64() - tz0;
       }
       const uint32_t slot = g % (uint32_t)R;
       long long tw0 = tlog ? clock64() : 0;
-      mbar_wait(b_full + 8u * slot, (g / (uint32_t)R) & 1u);
+      SD_MARK(kround, t, 2, g);
+      ST_WAIT(b_full + 8u * slot, (g / (uint32_t)R) & 1u);
       if (tlog) c_mbar += clock64() - tw0;
       long long tc0 = tlog ? clock64() : 0;
       const uint32_t srec = s_ring + slot * SLOT;
@@ -366,13 +430,19 @@ __global__ void __launch_bounds__(32 * (S + 1), 1)
       // push this diagonal to the next plane's CTA (its slot is free once
       // that CTA consumed the diagonal RZ before), publish it globally
       if (push_next) {
-        if (gz >= (uint32_t)RZ)
-          mbar_wait(my_zempty + 8u * zslot, ((gz / (uint32_t)RZ) - 1u) & 1u);
+        if (gz >= (uint32_t)RZ) {
+          SD_MARK(kround, t, 3, gz);
+          ST_WAIT(my_zempty + 8u * zslot, ((gz / (uint32_t)RZ) - 1u) & 1u);
+        }
         if (ok) {
           const uint32_t a = nx_zbuf + zslot * 768u + 24u * (uint32_t)(ix - first);
 #pragma unroll
           for (int c = 0; c < 3; ++c) st_async_f64(a + 8u * c, res[c], nx_zfull + 8u * zslot);
         }
+        // the receiver's slot phase also waits for this arrival, so a warp
+        // whose segment is empty on this diagonal cannot run a phase ahead of
+        // the sender's empty-wait above (which would alias its parity)
+        if (lane == 0) mbar_arrive_remote(nx_zfull + 8u * zslot);
       }
       if (ok) {
         double* go = oplane + 3 * (o + j);
@@ -402,6 +472,7 @@ __global__ void __launch_bounds__(32 * (S + 1), 1)
       }
       if constexpr (S > 1) {
         long long tb0 = tlog ? clock64() : 0;
+        SD_MARK(kround, t, 4, 0);
         named_bar(1, 32 * S);
         if (tlog) c_bar += clock64() - tb0;
       }
@@ -419,7 +490,8 @@ __global__ void __launch_bounds__(32 * (S + 1), 1)
       e[6] = (unsigned long long)c_comp;
       e[7] = (unsigned long long)c_bar;
     }
-  } while (false);
+  }
+  SD_MARK(kr_last, -1, 9, 0);
   cluster.sync();  // no CTA leaves while a neighbour may still push into it
 }
 
@@ -444,7 +516,7 @@ static int launch_stencil_s(const cprb_stencil& T, const double* rhs, double* ou
     set[dev] = smem;
   }
   const int C = STENCIL_CLUSTER;
-  const int nclus = (T.nz + C - 1) / C;
+  int nclus = (T.nz + C - 1) / C;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nclus * C);
   cfg.blockDim = dim3(32 * (S + 1));
@@ -459,6 +531,25 @@ static int launch_stencil_s(const cprb_stencil& T, const double* rhs, double* ou
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 2;
+  // persistent grid: at most the clusters that can be resident together
+  static int maxc[64][2] = {{0}};
+  int& mc = maxc[dev][UPPER ? 1 : 0];
+  if (mc == 0) {
+    cudaLaunchConfig_t q = cfg;
+    q.numAttrs = 1;  // cluster dimension only
+    if (cudaOccupancyMaxActiveClusters(&mc, (void*)k_stencil<UPPER, S, false>, &q) != cudaSuccess ||
+        mc < 1) {
+      cudaGetLastError();
+      mc = nsm[dev] / (2 * C) > 0 ? nsm[dev] / (2 * C) : 1;  // conservative fallback
+    }
+  }
+  if (nclus > mc) nclus = mc;
+  // test hook: fewer clusters, so each takes several rounds
+  if (const char* e = std::getenv("CPRB_STENCIL_MAXCLUS")) {
+    const int cap = std::atoi(e);
+    if (cap > 0 && nclus > cap) nclus = cap;
+  }
+  cfg.gridDim = dim3(nclus * C);
   if (g_stencil_log_on)
     cudaLaunchKernelEx(&cfg, k_stencil<UPPER, S, true>, T, rhs, out, ticket);
   else
@@ -492,6 +583,13 @@ int stencil_solve(const cprb_bilu& F, const double* rhsL, cudaStream_t st) {
 }
 
 }  // namespace cprb
+
+#ifdef STENCIL_DIAG
+extern "C" int cprb_stencil_set_diag(int* p) {
+  cudaMemcpyToSymbol(cprb::g_sdiag, &p, sizeof(p));
+  return cprb::check_launch("stencil diag");
+}
+#endif
 
 extern "C" int cprb_stencil_set_log(uint64_t* dev_log) {
   unsigned long long* p = (unsigned long long*)dev_log;

@@ -529,7 +529,9 @@ class DeviceBilu:
         self.use_wave = bool(F.n > 0 and use_wave)
         st = None
         if self.use_wave and os.environ.get("CPRB_STENCIL", "1") != "0":
-            st = F.stencil_device() if isinstance(F, DeviceBiluFactors) else stencil_plan(F)
+            dev_pack = (isinstance(F, DeviceBiluFactors)
+                        and os.environ.get("CPRB_DEVICE_STENCIL", "1") != "0")
+            st = F.stencil_device() if dev_pack else stencil_plan(F)
         self.stencil = st is not None
         if self.use_wave:
             # the wave plans carry their own copies of the factors; the

@@ -145,6 +145,29 @@ def test_stencil_kernel_bitwise_oracle_and_wave(gpu, shape, monkeypatch):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("shape,clusters", [((40, 7, 33), 1), ((70, 9, 20), 1), ((100, 5, 30), 1),
+                                            ((128, 3, 25), 1), ((70, 9, 40), 2), ((33, 6, 17), 3)])
+def test_stencil_persistent_rounds_bitwise(gpu, shape, clusters, monkeypatch):
+    """Persistent clusters taking several rounds of 8 planes each (the grid is
+    capped below nz / 8 clusters), S = 2..4 lane segments.  Exercises the
+    DSMEM hand-off across rounds, where a warp whose segment is empty on a
+    diagonal used to run a barrier phase ahead of its sender and hang."""
+    import torch
+    monkeypatch.setenv("CPRB_STENCIL_MAXCLUS", str(clusters))
+    F = P.bilu0_factorize(_grid(*shape, seed=1))
+    dev = F.device()
+    assert dev.stencil
+    Fo = _oracle_bilu(F)
+    rng = np.random.default_rng(11)
+    for _ in range(3):
+        r = rng.standard_normal(3 * F.n)
+        rd = torch.from_numpy(r).cuda()
+        z = torch.empty_like(rd)
+        dev.apply(rd, z)
+        assert np.array_equal(z.cpu().numpy(), orc.bilu_apply(Fo, r))
+
+
+@pytest.mark.gpu
 def test_stencil_cpr_solve_c1_matches_wave(gpu, monkeypatch):
     """A whole CPR-GMRES solve through the stencil BILU equals the one through
     the general wavefront bit for bit (same factors, same arithmetic)."""
