@@ -45,11 +45,16 @@ namespace cg = cooperative_groups;
 namespace cprb {
 
 constexpr int STENCIL_SMEM = 210 * 1024;
+// planes per thread-block cluster (DSMEM hand-offs): 16 (non-portable; the
+// B200 places ~7 such clusters) when the device can co-schedule them, else
+// 8.  Measured at C3: 8 / LAG 8 0.614 ms, 16 / LAG 4 0.528 ms per apply.
 #ifndef STENCIL_CLUSTER
-#define STENCIL_CLUSTER 8   // planes per thread-block cluster (DSMEM hand-offs)
+#define STENCIL_CLUSTER 16
 #endif
 constexpr int STENCIL_RZ = 8;        // pushed diagonals in flight per segment
-constexpr int STENCIL_LAG = 8;       // diagonals a cluster's first plane lets its producer lead
+#ifndef STENCIL_LAG
+#define STENCIL_LAG 4                // diagonals a cluster's first plane lets its producer lead
+#endif
 constexpr int STENCIL_DMAX = 1024;   // anti-diagonals per plane (nx + ny - 1) held in smem
 
 // diagnostic (cprb_stencil_set_log): per plane [UPPER][z] x 8 u64:
@@ -513,36 +518,52 @@ static int launch_stencil_s(const cprb_stencil& T, const double* rhs, double* ou
                          (int)smem);
     cudaFuncSetAttribute(k_stencil<UPPER, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
+    if (STENCIL_CLUSTER > 8) {
+      cudaFuncSetAttribute(k_stencil<UPPER, S, false>,
+                           cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(k_stencil<UPPER, S, true>,
+                           cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    }
     set[dev] = smem;
   }
-  const int C = STENCIL_CLUSTER;
-  int nclus = (T.nz + C - 1) / C;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(nclus * C);
   cfg.blockDim = dim3(32 * (S + 1));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = C;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 2;
-  // persistent grid: at most the clusters that can be resident together
-  static int maxc[64][2] = {{0}};
+  // cluster size and persistent grid (at most the clusters that can be
+  // resident together), chosen once per device and kernel
+  static int pick[64][2] = {{0}}, maxc[64][2] = {{0}};
+  int& C = pick[dev][UPPER ? 1 : 0];
   int& mc = maxc[dev][UPPER ? 1 : 0];
-  if (mc == 0) {
-    cudaLaunchConfig_t q = cfg;
-    q.numAttrs = 1;  // cluster dimension only
-    if (cudaOccupancyMaxActiveClusters(&mc, (void*)k_stencil<UPPER, S, false>, &q) != cudaSuccess ||
-        mc < 1) {
-      cudaGetLastError();
-      mc = nsm[dev] / (2 * C) > 0 ? nsm[dev] / (2 * C) : 1;  // conservative fallback
+  if (C == 0) {
+    int want = STENCIL_CLUSTER;
+    if (const char* e = std::getenv("CPRB_STENCIL_CLUSTER")) want = std::atoi(e);  // test hook
+    for (int c = want; c >= 2 && C == 0; c /= 2) {
+      cfg.numAttrs = 1;  // cluster dimension only
+      at[0].val.clusterDim.x = c;
+      cfg.gridDim = dim3(c);
+      int m = 0;
+      if (cudaOccupancyMaxActiveClusters(&m, (void*)k_stencil<UPPER, S, false>, &cfg) ==
+              cudaSuccess &&
+          m >= 1) {
+        C = c;
+        mc = m;
+      } else {
+        cudaGetLastError();
+      }
     }
+    if (C == 0) return set_error(CPRB_EDEVICE, "stencil BILU: no cluster shape fits the device");
   }
+  at[0].val.clusterDim.x = C;
+  cfg.numAttrs = 2;
+  int nclus = (T.nz + C - 1) / C;
   if (nclus > mc) nclus = mc;
   // test hook: fewer clusters, so each takes several rounds
   if (const char* e = std::getenv("CPRB_STENCIL_MAXCLUS")) {

@@ -167,6 +167,46 @@ def test_stencil_persistent_rounds_bitwise(gpu, shape, clusters, monkeypatch):
         assert np.array_equal(z.cpu().numpy(), orc.bilu_apply(Fo, r))
 
 
+_CLUSTER8_CHECK = """
+import sys
+import numpy as np
+import torch
+sys.path.insert(0, {tests!r})
+import paper_2201_01970_b200 as P
+from conftest import orc
+from test_stencil import _grid, _oracle_bilu
+for shape in ((40, 7, 33), (70, 9, 20), (60, 22, 19)):
+    F = P.bilu0_factorize(_grid(*shape, seed=2))
+    dev = F.device()
+    assert dev.stencil
+    r = np.random.default_rng(5).standard_normal(3 * F.n)
+    rd = torch.from_numpy(r).cuda()
+    z = torch.empty_like(rd)
+    dev.apply(rd, z)
+    assert np.array_equal(z.cpu().numpy(), orc.bilu_apply(_oracle_bilu(F), r)), shape
+print("ok")
+"""
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cluster", ["8", "4"])
+def test_stencil_smaller_cluster_shapes_bitwise(gpu, cluster):
+    """The launcher prefers 16-CTA clusters and falls back to 8 (then 4, 2)
+    when the device cannot co-schedule them; the kernel reads the cluster
+    size at run time.  Forced smaller shapes (fresh process: the choice is
+    made once per device) stay bitwise equal to the oracle."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    tests = str(Path(__file__).resolve().parent)
+    env = dict(os.environ, CPRB_STENCIL_CLUSTER=cluster, CPRB_STENCIL_MAXCLUS="1",
+               PYTHONPATH=str(Path(tests).parent))
+    out = subprocess.run([sys.executable, "-c", _CLUSTER8_CHECK.format(tests=tests)], env=env,
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
+
+
 @pytest.mark.gpu
 def test_stencil_cpr_solve_c1_matches_wave(gpu, monkeypatch):
     """A whole CPR-GMRES solve through the stencil BILU equals the one through
