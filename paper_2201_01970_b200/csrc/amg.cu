@@ -18,6 +18,21 @@ namespace cprb {
 
 static inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
+// where the V-cycle kernels let the next launch start (PDL): at entry
+// (default) or after their own dependency wait (-DPDL_LATE)
+#ifdef PDL_LATE
+#define PDL_EARLY_TRIGGER()
+#define PDL_LATE_TRIGGER() pdl_trigger()
+#else
+#define PDL_EARLY_TRIGGER() pdl_trigger()
+#define PDL_LATE_TRIGGER()
+#endif
+// widest register-prefetch template of a colour sweep (rows longer than it
+// stream the rest of the row, same summation order)
+#ifndef SWEEP_PRE_MAX
+#define SWEEP_PRE_MAX 32
+#endif
+
 // PGS-SCM colour update (src/smoothers.py:106-115):
 //   x_i = (b_i - sum_{stored off-diagonals, ascending permuted col} a_ij x_j) / d_i
 // ZG: zero initial guess -> only the prefix of entries whose columns precede
@@ -96,7 +111,7 @@ __global__ void __launch_bounds__(256, SWEEP_MINB)
             double* b, const double* __restrict__ gsrc, int gstride,
             const int32_t* __restrict__ perm, const double* xin, double* xout,
             double* __restrict__ sout) {
-  pdl_trigger();
+  PDL_EARLY_TRIGGER();
   AmgMark mk;
   mk.start(1 + ZG);
   const int w = s0 + (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
@@ -125,6 +140,7 @@ __global__ void __launch_bounds__(256, SWEEP_MINB)
       }
   }
   pdl_wait();
+  PDL_LATE_TRIGGER();
   mk.waited();
   if (!active) return;
   double bi;
@@ -271,7 +287,7 @@ __global__ void __launch_bounds__(256, PRE <= 8 ? 6 : (PRE <= 16 ? 4 : 2))
     k_resid_restrict(const cprb_sell R, const double* __restrict__ b,
                      const double* __restrict__ x, double* __restrict__ bc,
                      double* __restrict__ xn, const double* __restrict__ dn, int c0_rows) {
-  pdl_trigger();
+  PDL_EARLY_TRIGGER();
   AmgMark mk;
   mk.start(3);
   const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
@@ -295,6 +311,7 @@ __global__ void __launch_bounds__(256, PRE <= 8 ? 6 : (PRE <= 16 ? 4 : 2))
       }
   }
   pdl_wait();
+  PDL_LATE_TRIGGER();
   mk.waited();
   if (!wok) return;
   double res = 0.0;
@@ -341,12 +358,13 @@ static void launch_rr(const cprb_amg_level& L, const double* b, const double* x,
 // prolongation-correct x += ec[agg]  (src/amg.py:264)
 __global__ void k_prolong(int n, const int32_t* __restrict__ aggp, const double* __restrict__ xc,
                           double* __restrict__ x) {
-  pdl_trigger();
+  PDL_EARLY_TRIGGER();
   AmgMark mk;
   mk.start(4);
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int a = i < n ? __ldg(aggp + i) : 0;
   pdl_wait();
+  PDL_LATE_TRIGGER();
   mk.waited();
   if (i < n) x[i] = x[i] + xc[a];
   mk.end();
@@ -398,8 +416,12 @@ static void launch_sweep(const cprb_amg_level& L, int k, double* b, const double
                          double* sout, cudaStream_t st) {
   const int s0 = L.color_slices[k], s1 = L.color_slices[k + 1];
   if (s1 <= s0) return;
-  const int threads = (s1 - s0) * 32 >= 256 ? 256 : 128;
-  const int width = L.color_width ? L.color_width[2 * k + (ZG ? 1 : 0)] : 8;
+  // rows wider than 8 take the register-heavy templates: small blocks let
+  // more warps share an SM (measured at C3: V-cycle 703 -> 673 us)
+  const int wq = L.color_width ? L.color_width[2 * k + (ZG ? 1 : 0)] : 8;
+  const int threads = wq > 8 ? 64 : ((s1 - s0) * 32 >= 256 ? 256 : 128);
+  int width = L.color_width ? L.color_width[2 * k + (ZG ? 1 : 0)] : 8;
+  if (width > SWEEP_PRE_MAX) width = SWEEP_PRE_MAX;
   const int grid = nblk((int64_t)(s1 - s0) * 32, threads);
   auto go = [&](auto kern) {
     launch_pdl(kern, grid, threads, 0, st, L.smoother, s0, s1, L.color_rows[k],

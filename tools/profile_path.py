@@ -3,6 +3,7 @@
     python tools/profile_path.py [--what apply|spmv|bilu|vcycle|solve] [--reps N] [--grid 60,220,85]
 """
 import argparse
+import os
 import sys
 import time
 from pathlib import Path
@@ -97,6 +98,8 @@ def main():
         names = {1: "sweep", 2: "sweepZG", 3: "rr", 4: "prol"}
         tot = (L[-1, 3] - t0) / 1e3
         print("launches", len(L), "span us", tot)
+        if os.environ.get("AMGTL_OUT"):
+            np.save(os.environ["AMGTL_OUT"], L)
         gaps = (L[1:, 1] - L[:-1, 3]) / 1e3
         waits = (L[:, 2] - L[:, 1]) / 1e3
         work = (L[:, 3] - L[:, 2]) / 1e3
