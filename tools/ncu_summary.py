@@ -81,16 +81,23 @@ if lst.exists():
     hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
     h = rows[hi]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    mi = h.index("Metric Name") if "Metric Name" in h else None
     tot, cnt = defaultdict(float), Counter()
+    # SETUP kernels (device factorisation, packing, generator) run before the
+    # solves in the same process; the table is about the SOLVE path
+    setup = ("k_bilu_level", "k_stencil_pack", "k_pack_", "k_gen_", "k_fill", "k_sell_",
+             "k_factor", "k_scatter_vals", "k_uinv")
     for r in rows[hi + 1:]:
-        if len(r) <= vi:
+        if len(r) <= vi or (mi is not None and r[mi] != "gpu__time_duration.sum"):
             continue
         v = float(r[vi].replace(",", "")) * SCALE.get(r[ui], 1e-9) * 1e6
         nm = r[ki].split("(")[0].replace("void ", "").replace("cprb::", "")[:40]
+        if nm.startswith(setup):
+            continue
         tot[nm] += v
         cnt[nm] += 1
     T = sum(tot.values())
-    lines += ["", "## Launch list: one warm-up + one timed C3 solve (`ncu --metrics gpu__time_duration.sum`)",
+    lines += ["", "## Launch list: one warm-up + one timed C3 solve (`ncu --metrics gpu__time_duration.sum`; setup kernels excluded)",
               "", f"{sum(cnt.values())} launches, {T / 1e3:.2f} ms summed (serialised, cold caches).", "",
               "| kernel | launches | summed us | share |", "|---|---|---|---|"]
     for k, v in sorted(tot.items(), key=lambda x: -x[1])[:16]:

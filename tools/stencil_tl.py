@@ -42,3 +42,16 @@ for u in (0, 1):
         x = e[zz]
         D = x[5]
         print(f"  plane {zz:3d}: {(x[0]-t0)/1e3:7.1f} {(x[1]-t0)/1e3:7.1f}  tot {x[4]/D:6.0f}/diag  mbar {x[2]/D:5.0f}  z {x[3]/D:5.0f}  comp {x[6]/D:5.0f}  bar {x[7]/D:5.0f}")
+
+if os.environ.get("ALL"):
+    for u in (0, 1):
+        e = a[u, :nz]
+        t0 = e[:, 0].min()
+        order = range(nz) if u == 0 else range(nz - 1, -1, -1)
+        ends = [(e[z, 1] - t0) / 1e3 for z in order]
+        starts = [(e[z, 0] - t0) / 1e3 for z in order]
+        print("LU"[u], "end us by processing order:", " ".join(f"{v:.0f}" for v in ends))
+        print("LU"[u], "start us:", " ".join(f"{v:.0f}" for v in starts))
+        zc = [e[z, 3] / e[z, 5] for z in order]
+        print("LU"[u], "z-wait cycles/diag:", " ".join(f"{v:.0f}" for v in zc))
+
