@@ -37,6 +37,21 @@ def test_abi_exports_every_header_symbol():
     assert lib.cprb_version() >= 1
 
 
+def test_library_has_no_unresolved_internal_symbols():
+    """A shared library links with undefined symbols; a missing definition of
+    one of the package's own C++ functions would only fail when loaded on the
+    GPU box.  Every undefined symbol must come from the CUDA runtime / libc."""
+    import shutil
+    import subprocess
+    nm = shutil.which("nm")
+    if nm is None:
+        pytest.skip("nm not available")
+    out = subprocess.run([nm, "-D", "--undefined-only", str(N._LIB_PATH)], capture_output=True,
+                         text=True, check=True).stdout
+    bad = [ln for ln in out.splitlines() if "cprb" in ln]
+    assert not bad, bad
+
+
 def test_generator_bitwise_c1_and_sequence():
     g = load_golden("gen_c1.npz")
     (A, b), = P.generate_blackoil_like_sequence(10, 10, 10, 1, 0.01, 0).systems
