@@ -182,13 +182,16 @@ extern "C" int cprb_bilu_apply(const cprb_bilu* F, const double* r, double* z, d
   // arm the L output with the sentinel (the stage-2 kernel does this inside CPR)
   const int64_t n = (int64_t)F->n * F->b;
   if (n == 0) return CPRB_OK;
-  int rc = fill_sentinel(work_l, n, st);
-  if (rc) return rc;
+  int rc;
   if (F->use_wave) {
-    // the solves poll their own step-ordered outputs
-    rc = fill_sentinel(F->zl_step, F->len_l, st);
-    if (rc) return rc;
-    rc = fill_sentinel(F->y_step, F->len_u, st);
+    // the solves poll their own step-ordered outputs (the stencil solves
+    // only the planes a round reads from global memory)
+    if (F->use_wave == 2) {
+      rc = stencil_arm(*F, st);
+    } else {
+      rc = fill_sentinel(F->zl_step, F->len_l, st);
+      if (!rc) rc = fill_sentinel(F->y_step, F->len_u, st);
+    }
     if (rc) return rc;
     rc = wave_scatter_rhs(*F, r, F->rhs_l, st);
     if (rc) return rc;
@@ -196,5 +199,7 @@ extern "C" int cprb_bilu_apply(const cprb_bilu* F, const double* r, double* z, d
     if (rc) return rc;
     return wave_combine(*F, nullptr, z, st);
   }
+  rc = fill_sentinel(work_l, n, st);
+  if (rc) return rc;
   return bilu_solve(*F, r, work_l, z, nullptr, nullptr, st);
 }

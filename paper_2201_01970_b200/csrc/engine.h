@@ -37,6 +37,7 @@ int bsr_op(int mode, const cprb_sell& A, int b, const double* x, const double* r
            const int32_t* sent2_idx = nullptr);
 int wave_solve(const cprb_bilu& F, const double* rhsL, cudaStream_t st);
 int stencil_solve(const cprb_bilu& F, const double* rhsL, cudaStream_t st);
+int stencil_arm(const cprb_bilu& F, cudaStream_t st);
 int wave_combine(const cprb_bilu& F, const double* zp, double* z, cudaStream_t st);
 int wave_scatter_rhs(const cprb_bilu& F, const double* r, double* rhsL, cudaStream_t st);
 int amg_vcycle(const cprb_amg& h, const double* r, double* z, cudaStream_t st);

@@ -232,8 +232,15 @@ int cprb_cpr_finish(const cprb_cpr* P, const double* r, double* z, void* stream)
   if (F.use_wave) {
     // stage-2 residual written straight into the L plan's step order; it
     // also arms the step-ordered outputs the L and U solves poll
-    int rc = bsr_op(2, P->A, P->b, P->zp, r, F.rhs_l, nullptr, F.zl_step, st, F.l_slot, F.y_step,
-                    F.l_slot, F.u_slot);
+    int rc;
+    if (F.use_wave == 2) {
+      // stencil solves: arm only the planes a round polls (csrc/stencil.cu)
+      rc = bsr_op(2, P->A, P->b, P->zp, r, F.rhs_l, nullptr, nullptr, st, F.l_slot);
+      if (!rc) rc = stencil_arm(F, st);
+    } else {
+      rc = bsr_op(2, P->A, P->b, P->zp, r, F.rhs_l, nullptr, F.zl_step, st, F.l_slot, F.y_step,
+                  F.l_slot, F.u_slot);
+    }
     if (rc) return rc;
     // the solves publish in step order (coalesced); z = Pi zp + y is one
     // gather pass afterwards

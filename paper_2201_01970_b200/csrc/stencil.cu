@@ -511,71 +511,96 @@ __global__ void __launch_bounds__(32 * (S + 1), 1)
   cluster.sync();  // no CTA leaves while a neighbour may still push into it
 }
 
+// Per device and kernel: dynamic shared memory opt-in, the cluster size
+// (16 when the device co-schedules such clusters, else 8, 4, 2) and the
+// number of clusters that can be resident together.  Returns 0 on failure.
+struct StencilShape {
+  int C = 0, maxc = 0;
+  size_t smem = 0;
+};
 template <bool UPPER, int S>
-static int launch_stencil_s(const cprb_stencil& T, const double* rhs, double* out, int32_t* ticket,
-                            cudaStream_t st) {
+static StencilShape stencil_shape() {
   constexpr int NF = stencil_nf<UPPER>();
   constexpr int R = stencil_ring(NF, S);
-  if (T.D > STENCIL_DMAX) return set_error(CPRB_EUNSUPPORTED, "stencil BILU: nx + ny too large");
   const size_t smem = (size_t)R * stencil_slot_bytes(NF, S) + stencil_fixed_bytes(S);
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) dev = 0;
-  static int nsm[64] = {0};
-  static size_t set[64] = {0};
-  if (!nsm[dev]) cudaDeviceGetAttribute(&nsm[dev], cudaDevAttrMultiProcessorCount, dev);
-  if (smem > set[dev]) {
-    cudaFuncSetAttribute(k_stencil<UPPER, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    cudaFuncSetAttribute(k_stencil<UPPER, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    if (STENCIL_CLUSTER > 8) {
-      cudaFuncSetAttribute(k_stencil<UPPER, S, false>,
-                           cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      cudaFuncSetAttribute(k_stencil<UPPER, S, true>,
-                           cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    }
-    set[dev] = smem;
+  static StencilShape cache[64];
+  StencilShape& sh = cache[dev];
+  if (sh.C) return sh;
+  cudaFuncSetAttribute(k_stencil<UPPER, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  cudaFuncSetAttribute(k_stencil<UPPER, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  if (STENCIL_CLUSTER > 8) {
+    cudaFuncSetAttribute(k_stencil<UPPER, S, false>, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                         1);
+    cudaFuncSetAttribute(k_stencil<UPPER, S, true>, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                         1);
   }
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(32 * (S + 1));
   cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int want = STENCIL_CLUSTER;
+  if (const char* e = std::getenv("CPRB_STENCIL_CLUSTER")) want = std::atoi(e);  // test hook
+  for (int c = want; c >= 2 && sh.C == 0; c /= 2) {
+    at[0].val.clusterDim.x = c;
+    cfg.gridDim = dim3(c);
+    int m = 0;
+    if (cudaOccupancyMaxActiveClusters(&m, (void*)k_stencil<UPPER, S, false>, &cfg) ==
+            cudaSuccess &&
+        m >= 1) {
+      sh.C = c;
+      sh.maxc = m;
+    } else {
+      cudaGetLastError();
+    }
+  }
+  sh.smem = smem;
+  return sh;
+}
+
+template <bool UPPER>
+static int stencil_cluster_size(int S) {
+  switch (S) {
+    case 1: return stencil_shape<UPPER, 1>().C;
+    case 2: return stencil_shape<UPPER, 2>().C;
+    case 3: return stencil_shape<UPPER, 3>().C;
+    case 4: return stencil_shape<UPPER, 4>().C;
+    default: return 0;
+  }
+}
+
+template <bool UPPER, int S>
+static int launch_stencil_s(const cprb_stencil& T, const double* rhs, double* out, int32_t* ticket,
+                            cudaStream_t st) {
+  if (T.D > STENCIL_DMAX) return set_error(CPRB_EUNSUPPORTED, "stencil BILU: nx + ny too large");
+  const StencilShape sh = stencil_shape<UPPER, S>();
+  if (sh.C == 0) return set_error(CPRB_EDEVICE, "stencil BILU: no cluster shape fits the device");
+  const int C = sh.C;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(32 * (S + 1));
+  cfg.dynamicSmemBytes = sh.smem;
   cfg.stream = st;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = C;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  // cluster size and persistent grid (at most the clusters that can be
-  // resident together), chosen once per device and kernel
-  static int pick[64][2] = {{0}}, maxc[64][2] = {{0}};
-  int& C = pick[dev][UPPER ? 1 : 0];
-  int& mc = maxc[dev][UPPER ? 1 : 0];
-  if (C == 0) {
-    int want = STENCIL_CLUSTER;
-    if (const char* e = std::getenv("CPRB_STENCIL_CLUSTER")) want = std::atoi(e);  // test hook
-    for (int c = want; c >= 2 && C == 0; c /= 2) {
-      cfg.numAttrs = 1;  // cluster dimension only
-      at[0].val.clusterDim.x = c;
-      cfg.gridDim = dim3(c);
-      int m = 0;
-      if (cudaOccupancyMaxActiveClusters(&m, (void*)k_stencil<UPPER, S, false>, &cfg) ==
-              cudaSuccess &&
-          m >= 1) {
-        C = c;
-        mc = m;
-      } else {
-        cudaGetLastError();
-      }
-    }
-    if (C == 0) return set_error(CPRB_EDEVICE, "stencil BILU: no cluster shape fits the device");
-  }
-  at[0].val.clusterDim.x = C;
   cfg.numAttrs = 2;
+  // persistent grid: at most the clusters that can be resident together
   int nclus = (T.nz + C - 1) / C;
-  if (nclus > mc) nclus = mc;
+  if (nclus > sh.maxc) nclus = sh.maxc;
   // test hook: fewer clusters, so each takes several rounds
   if (const char* e = std::getenv("CPRB_STENCIL_MAXCLUS")) {
     const int cap = std::atoi(e);
@@ -591,6 +616,37 @@ static int launch_stencil_s(const cprb_stencil& T, const double* rhs, double* ou
   else
     cudaLaunchKernelEx(&cfg, k_stencil<UPPER, S, false>, T, rhs, out, ticket);
   return check_launch("stencil bilu");
+}
+
+// The only rows the solves poll are those of the plane a round's first
+// plane reads from global memory: the last plane of every earlier round
+// (processing order zt = kC - 1).  Arm just those planes with the sentinel
+// instead of the whole L / U outputs (2 x 27 MB at C3).
+__global__ void k_arm_planes(double* zl, double* yu, int64_t P3, int nz, int CL, int CU,
+                             int nl, int nu) {
+  const int k = blockIdx.y;  // plane ordinal
+  const bool upper = k >= nl;
+  const int i = upper ? k - nl : k;
+  const int zt = (i + 1) * (upper ? CU : CL) - 1;
+  const int z = upper ? nz - 1 - zt : zt;
+  double* base = (upper ? yu : zl) + (int64_t)z * P3;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < P3;
+       e += (int64_t)gridDim.x * blockDim.x)
+    base[e] = __longlong_as_double((long long)CPRB_SENTINEL);
+}
+
+int stencil_arm(const cprb_bilu& F, cudaStream_t st) {
+  const cprb_stencil& T = F.St;
+  const int CL = stencil_cluster_size<false>(T.S), CU = stencil_cluster_size<true>(T.S);
+  if (CL == 0 || CU == 0) return set_error(CPRB_EDEVICE, "stencil BILU: no cluster shape fits the device");
+  // round k >= 1 reads plane kC - 1 (processing order); rounds exist while kC < nz
+  const int nl = (T.nz + CL - 1) / CL - 1, nu = (T.nz + CU - 1) / CU - 1;
+  const int tot = nl + nu;
+  if (tot <= 0) return CPRB_OK;
+  const int64_t P3 = (int64_t)T.P * 3;
+  const int bx = (int)((P3 + 255) / 256 < 64 ? (P3 + 255) / 256 : 64);
+  k_arm_planes<<<dim3(bx, tot), 256, 0, st>>>(F.zl_step, F.y_step, P3, T.nz, CL, CU, nl, nu);
+  return check_launch("stencil arm");
 }
 
 template <bool UPPER>
