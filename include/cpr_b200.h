@@ -389,6 +389,19 @@ int cprb_div_host(int64_t n, const double* x, double h, double* out, void* strea
 /* out = x / (*h_dev)  (src/cpr.py:262 V[0] = r / beta) */
 int cprb_div_scalar(int64_t n, const double* x, const double* h_dev, double* out, void* stream);
 
+/* src/cpr.py:231-316  restarted right-preconditioned GMRES driven in C++
+ * (for hosts without Python): solves A x = rhs from the initial guess in x
+ * (dev, overwritten by the solution).  P: CPR preconditioner or NULL;
+ * graphs: cprb_graph_cache_create cache or NULL (plain launches).
+ * work: dev doubles, >= (m+1)*n + 3*n + 2*m + 3 + CPRB_RED_BLOCKS;
+ * iwork: dev int32[4].  result[4] out (host): outer, inner, converged (0/1),
+ * rel_residual.  Same steps and stopping rules as the Python driver; the
+ * triangular solve is a plain back substitution (x agrees with the Python
+ * driver to rounding); a zero Hessenberg pivot returns CPRB_EUNSUPPORTED. */
+int cprb_gmres_solve(const cprb_sell* A, int32_t b, const cprb_cpr* P, void* graphs, int64_t n,
+                     const double* rhs, double* x, int32_t m, int32_t max_restarts, double tol,
+                     double* work, int32_t* iwork, double* result, void* stream);
+
 /* Device SELL-32 packing of a (block) CSR matrix in natural row order
  * (uploads of new Jacobians, src/sparse.py:203-308 layout -> cprb_sell):
  * row_ptr/col_idx int64 and values (nnz*b*b) are device copies of the CSR

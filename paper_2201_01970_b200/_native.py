@@ -146,6 +146,8 @@ _SIGS = {
     "cprb_add": (C.c_int, [C.c_int64, vp, vp, vp, vp]),
     "cprb_axpy": (C.c_int, [C.c_int64, C.c_double, vp, vp, vp, vp]),
     "cprb_div_scalar": (C.c_int, [C.c_int64, vp, vp, vp, vp]),
+    "cprb_gmres_solve": (C.c_int, [vp, C.c_int32, vp, vp, C.c_int64, vp, vp, C.c_int32, C.c_int32,
+                                   C.c_double, vp, vp, vp, vp]),
 }
 
 # every symbol include/cpr_b200.h declares (checked by tests/test_native_abi.py)

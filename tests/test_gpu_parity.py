@@ -547,3 +547,48 @@ def test_c4_sequence_rebuild_mix_against_reference(gpu):
     for r, xs in zip(out.records, ref["x_sample"]):
         xs = np.asarray(xs)
         assert np.linalg.norm(r.x[::st] - xs) <= 1e-6 * np.linalg.norm(xs)
+
+
+def test_c_abi_gmres_driver_matches_python_driver(gpu):
+    """cprb_gmres_solve (the whole restarted GMRES driven in C++, for hosts
+    without Python) takes the same steps as gmres_solve: equal iteration
+    counts and convergence, x and the relative residual equal to rounding."""
+    import ctypes as C
+    import torch
+    from paper_2201_01970_b200 import _native as N
+    from paper_2201_01970_b200 import device as D
+    (A, b), = P.generate_blackoil_like_sequence(16, 12, 9, 1, 0.01, 3).systems
+    for cycle in ("v", "k"):
+        cfg = P.SolverConfig(theta=0.0, theta_amg=0.0, cycle=cycle)
+        B = P.build_cpr(A, cfg)
+        ref = P.gmres_solve(A, b, None, B, cfg.gmres_params())
+        Bd = B.device()
+        M = D.device_matrix(A)
+        prm = cfg.gmres_params()
+        n = b.shape[0]
+        m = prm.m
+        work = torch.zeros((m + 1) * n + 3 * n + 2 * m + 3 + 1184, dtype=torch.float64,
+                           device="cuda")
+        iwork = torch.zeros(4, dtype=torch.int32, device="cuda")
+        bd = torch.from_numpy(b).cuda()
+        x = torch.zeros(n, dtype=torch.float64, device="cuda")
+        res = (C.c_double * 4)()
+        desc = Bd.kdesc if cycle == "k" else Bd.desc   # the K-cycle's descriptor (set by apply)
+        N.check(N.lib().cprb_gmres_solve(C.addressof(M.sell.desc), 3, C.addressof(desc),
+                                         Bd.graphs, n, D.ptr(bd), D.ptr(x), m, prm.max_restarts,
+                                         prm.tol, D.ptr(work), D.ptr(iwork), res, D.stream()))
+        torch.cuda.synchronize()
+        assert (int(res[0]), int(res[1]), bool(res[2])) == (ref.outer, ref.inner, ref.converged)
+        assert abs(res[3] - ref.rel_residual) <= 1e-9 * ref.rel_residual
+        xr = np.asarray(ref.x)
+        assert np.linalg.norm(x.cpu().numpy() - xr) <= 1e-10 * np.linalg.norm(xr)
+    # unpreconditioned, and the dimension check
+    x.zero_()
+    N.check(N.lib().cprb_gmres_solve(C.addressof(M.sell.desc), 3, None, None, n, D.ptr(bd),
+                                     D.ptr(x), m, 2, 1e-30, D.ptr(work), D.ptr(iwork), res,
+                                     D.stream()))
+    torch.cuda.synchronize()
+    assert int(res[0]) == 2 and int(res[1]) == 2 * m and not bool(res[2])
+    assert N.lib().cprb_gmres_solve(C.addressof(M.sell.desc), 3, None, None, n - 3, D.ptr(bd),
+                                    D.ptr(x), m, 2, 1e-6, D.ptr(work), D.ptr(iwork), res,
+                                    D.stream()) == N.EINVAL
