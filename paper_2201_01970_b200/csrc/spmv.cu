@@ -63,8 +63,12 @@ __device__ __forceinline__ double bsr_row_long(const cprb_sell& A, int64_t base,
   return segsum_rt(f, B * len);
 }
 
+// resident CTAs per SM: the full products keep 5 (more spills their
+// register prefetch: 139 -> 145 / 180 us at 6 / 8); the stage-2 residual
+// (one value plane per block) is latency bound and gains from 8 (CPR
+// application 1268 -> 1241 us at C3)
 template <int B, int MODE>
-__global__ void __launch_bounds__(BSR_WARPS * 32, 5)
+__global__ void __launch_bounds__(BSR_WARPS * 32, MODE == 2 ? 8 : 5)
     k_bsr(const cprb_sell A, const double* __restrict__ x, const double* __restrict__ rhs,
           double* __restrict__ out, int32_t* flag, double* __restrict__ sent,
           double* __restrict__ sent2, const int32_t* __restrict__ out_idx,
