@@ -371,6 +371,11 @@ int cprb_cpr_finish(const cprb_cpr* P, const double* r, double* z, void* stream)
 int cprb_dot(int64_t n, const double* x, const double* y, double* out, double* partials,
              int32_t* ticket, void* stream);
 
+/* *out = sqrt((x, x)) on the device (same reduction as cprb_dot, IEEE sqrt):
+ * src/sparse.py:361-369 norm2 without a host round trip. */
+int cprb_norm2(int64_t n, const double* x, double* out, double* partials, int32_t* ticket,
+               void* stream);
+
 /* src/cpr.py:276-284  Arnoldi MGS for column j: for i<=j: H[i]=(w,V_i),
  * w -= H[i] V_i; H[j+1] = ||w||; V_{j+1} = w / H[j+1] (if nonzero).
  * V: (j+2) rows of length n (row stride ldv); w is V_{j+1} (in place). */

@@ -146,6 +146,7 @@ _SIGS = {
     "cprb_add": (C.c_int, [C.c_int64, vp, vp, vp, vp]),
     "cprb_axpy": (C.c_int, [C.c_int64, C.c_double, vp, vp, vp, vp]),
     "cprb_div_scalar": (C.c_int, [C.c_int64, vp, vp, vp, vp]),
+    "cprb_norm2": (C.c_int, [C.c_int64, vp, vp, vp, vp, vp]),
     "cprb_gmres_solve": (C.c_int, [vp, C.c_int32, vp, vp, C.c_int64, vp, vp, C.c_int32, C.c_int32,
                                    C.c_double, vp, vp, vp, vp]),
 }

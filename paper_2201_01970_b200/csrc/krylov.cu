@@ -182,6 +182,20 @@ int cprb_dot(int64_t n, const double* x, const double* y, double* out, double* p
   return check_launch("dot");
 }
 
+// *out = sqrt((x, x)) on the device: the same partition, tree and sqrt as
+// cprb_dot followed by a host sqrt (src/sparse.py:361-369), no host round trip
+int cprb_norm2(int64_t n, const double* x, double* out, double* partials, int32_t* ticket,
+               void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n <= 0) {
+    cudaMemsetAsync(out, 0, sizeof(double), st);
+    return check_launch("norm2");
+  }
+  k_mgs_stage<1><<<red_blocks(n), RED_THREADS, 0, st>>>(n, const_cast<double*>(x), nullptr,
+                                                          nullptr, nullptr, partials, ticket, out);
+  return check_launch("norm2");
+}
+
 int cprb_arnoldi_mgs(int64_t n, int32_t j, double* V, int64_t ldv, double* Hcol,
                      double* partials, int32_t* ticket, void* stream) {
   NvtxRange nv("arnoldi_mgs");
