@@ -50,6 +50,38 @@ __global__ void k_axpy_alpha(int n, const double* __restrict__ s, double sign,
     out[i] = a * x[i] + y[i];
 }
 
+// start of an FCG frame: active = 1, r = rhs, x = 0 (one launch instead of
+// a flag kernel, a memset and a copy)
+__global__ void k_fcg_start(int n, double* s, const double* __restrict__ rhs,
+                            double* __restrict__ r, double* __restrict__ x) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) s[S_ACTIVE] = 1.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    r[i] = rhs[i];
+    x[i] = 0.0;
+  }
+}
+
+// k_fcg_alpha + k_axpy_alpha(+1: x += alpha p) [+ k_axpy_alpha(-1: r -= alpha ap)]
+// in one launch: every thread evaluates the same predicate and quotient
+// (bitwise those of k_fcg_alpha); block 0 thread 0 records them in s
+__global__ void k_fcg_update(int n, double* s, int ip, const double* __restrict__ p,
+                             double* x, const double* __restrict__ ap, double* r) {
+  if (s[S_ACTIVE] == 0.0) return;
+  const double pap = s[ip];
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  if (pap <= 0.0 || !isfinite(pap)) {
+    if (lead) s[S_ACTIVE] = 0.0;
+    return;
+  }
+  const double alpha = s[S_PR] / pap;
+  if (lead) s[S_ALPHA] = alpha;
+  const double na = -1.0 * alpha;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    x[i] = (1.0 * alpha) * p[i] + x[i];
+    if (ap) r[i] = na * ap[i] + r[i];
+  }
+}
+
 // p = p - (dot(z, ap_j) / pap_j) p_j  ==  (-coef) * p_j + z
 __global__ void k_axpy_coef(int n, const double* __restrict__ s, const double* __restrict__ pj,
                             const double* __restrict__ z, double* __restrict__ out) {
@@ -229,9 +261,7 @@ static int fcg_at(const KPlan& P, const cprb_amg& h, int l, const double* rhs, c
   double* s = P.s[l];
   double *x = P.x[l], *r = P.r[l], *z1 = P.z1[l], *ap1 = P.ap1[l], *z2 = P.z2[l];
   double *p2 = P.p2[l], *ap2 = P.ap2[l];
-  k_fcg_init<<<1, 1, 0, st>>>(s);
-  cudaMemsetAsync(x, 0, sizeof(double) * n, st);
-  cudaMemcpyAsync(r, rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, st);
+  k_fcg_start<<<kb(n), 256, 0, st>>>(n, s, rhs, r, x);
   int rc;
   // step 1 (no stored directions: p = z)
   if ((rc = kdot(P, n, r, r, s + S_RR, st))) return rc;
@@ -240,9 +270,7 @@ static int fcg_at(const KPlan& P, const cprb_amg& h, int l, const double* rhs, c
   if ((rc = bsr_op(0, P.spmv[l], 1, z1, nullptr, ap1, nullptr, nullptr, st))) return rc;
   if ((rc = kdot(P, n, z1, ap1, s + S_PAP1, st))) return rc;
   if ((rc = kdot(P, n, z1, r, s + S_PR, st))) return rc;
-  k_fcg_alpha<<<1, 1, 0, st>>>(s, S_PAP1);
-  k_axpy_alpha<<<kb(n), 256, 0, st>>>(n, s, 1.0, z1, x, x);
-  k_axpy_alpha<<<kb(n), 256, 0, st>>>(n, s, -1.0, ap1, r, r);
+  k_fcg_update<<<kb(n), 256, 0, st>>>(n, s, S_PAP1, z1, x, ap1, r);
   // step 2 (one stored direction)
   if ((rc = kdot(P, n, r, r, s + S_RR, st))) return rc;
   k_fcg_check_rr<<<1, 1, 0, st>>>(s);
@@ -252,8 +280,8 @@ static int fcg_at(const KPlan& P, const cprb_amg& h, int l, const double* rhs, c
   if ((rc = bsr_op(0, P.spmv[l], 1, p2, nullptr, ap2, nullptr, nullptr, st))) return rc;
   if ((rc = kdot(P, n, p2, ap2, s + S_PAP2, st))) return rc;
   if ((rc = kdot(P, n, p2, r, s + S_PR, st))) return rc;
-  k_fcg_alpha<<<1, 1, 0, st>>>(s, S_PAP2);
-  k_axpy_alpha<<<kb(n), 256, 0, st>>>(n, s, 1.0, p2, x, x);
+  k_fcg_update<<<kb(n), 256, 0, st>>>(n, s, S_PAP2, p2, x, (const double*)nullptr,
+                                      (double*)nullptr);
   return check_launch("fcg");
 }
 
