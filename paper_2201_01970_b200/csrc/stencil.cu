@@ -51,7 +51,9 @@ constexpr int STENCIL_SMEM = 210 * 1024;
 #ifndef STENCIL_CLUSTER
 #define STENCIL_CLUSTER 16
 #endif
-constexpr int STENCIL_RZ = 8;        // pushed diagonals in flight per segment
+#ifndef STENCIL_RZ
+#define STENCIL_RZ 8                 // pushed diagonals in flight per segment
+#endif
 #ifndef STENCIL_LAG
 #define STENCIL_LAG 4                // diagonals a cluster's first plane lets its producer lead
 #endif
