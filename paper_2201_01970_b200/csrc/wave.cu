@@ -98,6 +98,15 @@ __device__ __forceinline__ bool is_sentinel(double v) {
   return (unsigned long long)__double_as_longlong(v) == CPRB_SENTINEL;
 }
 
+// Global dependencies may have been published by a peer GPU (slab path:
+// st.relaxed.sys into this rank's buffer), so they are read at system scope;
+// on one GPU this is the same L2 access as a gpu-scope relaxed load.
+__device__ __forceinline__ double ld_relaxed_sys(const double* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return __longlong_as_double((long long)v);
+}
+
 // all B components polled concurrently until none is the sentinel
 template <int B>
 __device__ __forceinline__ void wait_block(const double* g, double* v) {
@@ -111,7 +120,7 @@ __device__ __forceinline__ void wait_block(const double* g, double* v) {
     if (spins > (1 << 27)) __trap();  // a producer that never publishes: fail, do not hang
 #pragma unroll
     for (int c = 0; c < B; ++c)
-      if (is_sentinel(v[c])) v[c] = ld_relaxed(g + c);
+      if (is_sentinel(v[c])) v[c] = ld_relaxed_sys(g + c);
   }
 }
 
@@ -178,7 +187,7 @@ __device__ __forceinline__ void row_fast(uint32_t sblk, uint32_t srhs, int l, in
   for (int m = 0; m < K; ++m)
     if (m < len && code[m] >= 0)
 #pragma unroll
-      for (int c = 0; c < B; ++c) dv[m][c] = ld_relaxed(glob + (int64_t)code[m] + c);
+      for (int c = 0; c < B; ++c) dv[m][c] = ld_relaxed_sys(glob + (int64_t)code[m] + c);
   // in-chunk dependencies: poll all flags with relaxed loads, then one
   // acquire fence before reading the values (instead of one acquire each)
   uint32_t rslot[KA];
@@ -249,7 +258,7 @@ __device__ __noinline__ void row_general(const uint8_t* blk, int K, const double
         ring_value<B>(ring, k, -code - 1, dv);
       } else {
 #pragma unroll
-        for (int c = 0; c < B; ++c) dv[c] = ld_relaxed(glob + (int64_t)code + c);
+        for (int c = 0; c < B; ++c) dv[c] = ld_relaxed_sys(glob + (int64_t)code + c);
         wait_block<B>(glob + (int64_t)code, dv);
       }
       double mr[B];
