@@ -602,7 +602,7 @@ def _ncu_traffic(kernel: str, grid):
     e = d.get("kernels", {}).get(kernel)
     if not e:
         return None, None
-    return int(e["dram_bytes"]), d.get("source")
+    return int(e["dram_bytes"]), e.get("source") or d.get("source")
 
 
 def _count_launches(solve, torch):
